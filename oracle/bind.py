@@ -1,0 +1,324 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes bindings for the CPU checkers.
+
+* ``Oracle``    -> oracle/liboracle.so, the plain-C restatement
+                   (oracle/ranmar_oracle.c, each function citing the
+                   reference file:line it restates).
+* ``Reference`` -> oracle/_ref/libranmar_ref.so, the reference's own headers
+                   compiled in place by oracle/Makefile (optional: absent when
+                   /root/reference was never available to build it).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module. The product package
+(paper_2512_00093_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libranmar_ref.so")
+ACCEPTANCE_BIN = os.path.join(HERE, "_ref", "acceptance")
+
+# ranmar::RanmarState (core.hpp:29-49): 97 x u32 lanes, int i, int j, u32 v = 400 B.
+STATE_DTYPE = np.dtype([("lane", "<u4", (97,)), ("i", "<i4"), ("j", "<i4"), ("v", "<u4")])
+assert STATE_DTYPE.itemsize == 400
+# or_gauss_state: state + saved double + flag + pad = 416 B.
+GAUSS_DTYPE = np.dtype([("s", STATE_DTYPE), ("saved", "<f8"), ("has_saved", "<u4"), ("pad", "<u4")])
+assert GAUSS_DTYPE.itemsize == 416
+
+MASK = 0xFFFFFF
+ARITH_MOD = 16777213
+
+
+def j_limbs(j: int) -> np.ndarray:
+    """Python int -> 4 x u64 little-endian limbs (the C-ABI jump-count layout)."""
+    if j < 0 or j >= 1 << 256:
+        raise ValueError("jump count must be in [0, 2^256)")
+    return np.array([(j >> (64 * k)) & ((1 << 64) - 1) for k in range(4)], dtype=np.uint64)
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _build_hint() -> str:
+    return "run `make -C oracle` (or __graft_entry__.build())"
+
+
+class Oracle:
+    """The C restatement. All arrays are numpy, states use STATE_DTYPE."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing; {_build_hint()}")
+        self.lib = C.CDLL(path)
+        L = self.lib
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        sig = {
+            "or_init": (i32, [u32, vp]),
+            "or_init_unchecked": (None, [u32, vp]),
+            "or_step": (u32, [vp]),
+            "or_step_n": (None, [vp, u64, vp]),
+            "or_value_of": (i32, [u32, vp]),
+            "or_init_float": (i32, [u32, vp]),
+            "or_step_float_n": (None, [vp, u64, vp]),
+            "or_reduce_trinomial": (None, [vp, i32, vp]),
+            "or_mul_mod": (None, [vp, vp, vp]),
+            "or_mul_by_t": (None, [vp, vp]),
+            "or_pow_t_mod": (None, [vp, vp]),
+            "or_canonicalize": (None, [vp, vp]),
+            "or_apply_companion": (None, [vp, vp]),
+            "or_jump_fib": (None, [vp, vp, vp]),
+            "or_jump_arith": (u32, [u32, vp]),
+            "or_jump_state": (None, [vp, vp, vp]),
+            "or_make_streams": (i32, [vp, vp, u64, u64, vp]),
+            "or_j256_parse": (i32, [C.c_char_p, vp]),
+            "or_generate_u32": (None, [vp, u64, u64, vp]),
+            "or_generate_f32": (None, [vp, u64, u64, vp]),
+            "or_consume": (None, [vp, u64, u64, vp, vp]),
+            "or_gaussian_fill": (None, [vp, u64, u64, u64, vp]),
+            "or_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
+            "or_from_text": (i32, [C.c_char_p, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+
+    # -- core ---------------------------------------------------------------
+    def init(self, seed: int, checked: bool = True) -> np.ndarray:
+        s = np.zeros(1, STATE_DTYPE)
+        if checked:
+            if self.lib.or_init(seed, _p(s)) != 0:
+                raise ValueError("ranmar: seed must be in [0, 900000000]")
+        else:
+            self.lib.or_init_unchecked(seed, _p(s))
+        return s
+
+    def step_n(self, state: np.ndarray, n: int) -> np.ndarray:
+        """Advances `state` (1-element STATE_DTYPE array) in place; returns n u24 outputs."""
+        out = np.empty(n, np.uint32)
+        self.lib.or_step_n(_p(state), n, _p(out))
+        return out
+
+    def float_outputs(self, seed: int, n: int) -> np.ndarray:
+        st = (C.c_char * (97 * 8 + 8 + 8))()
+        if self.lib.or_init_float(seed, C.cast(st, C.c_void_p)) != 0:
+            raise ValueError("ranmar: seed must be in [0, 900000000]")
+        out = np.empty(n, np.float64)
+        self.lib.or_step_float_n(C.cast(st, C.c_void_p), n, _p(out))
+        return out
+
+    # -- polynomial ring ----------------------------------------------------
+    def pow_t_mod(self, j: int) -> np.ndarray:
+        out = np.empty(97, np.uint32)
+        self.lib.or_pow_t_mod(_p(j_limbs(j)), _p(out))
+        return out
+
+    def mul_mod(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        out = np.empty(97, np.uint32)
+        self.lib.or_mul_mod(_p(np.ascontiguousarray(a, np.uint32)),
+                            _p(np.ascontiguousarray(b, np.uint32)), _p(out))
+        return out
+
+    def reduce_trinomial(self, raw: np.ndarray) -> np.ndarray:
+        raw = np.ascontiguousarray(raw, np.uint32)
+        out = np.empty(97, np.uint32)
+        self.lib.or_reduce_trinomial(_p(raw), len(raw), _p(out))
+        return out
+
+    # -- jump ---------------------------------------------------------------
+    def canonicalize(self, state: np.ndarray) -> np.ndarray:
+        out = np.empty(97, np.uint32)
+        self.lib.or_canonicalize(_p(state), _p(out))
+        return out
+
+    def jump_state(self, state: np.ndarray, j: int) -> np.ndarray:
+        out = np.zeros(1, STATE_DTYPE)
+        self.lib.or_jump_state(_p(np.ascontiguousarray(state)), _p(j_limbs(j)), _p(out))
+        return out
+
+    def jump_arith(self, v: int, j: int) -> int:
+        return int(self.lib.or_jump_arith(v, _p(j_limbs(j))))
+
+    def make_streams(self, base: np.ndarray, j: int, n: int, first: int = 0) -> np.ndarray:
+        out = np.zeros(n, STATE_DTYPE)
+        if self.lib.or_make_streams(_p(np.ascontiguousarray(base)), _p(j_limbs(j)), first, n,
+                                    _p(out)) != 0:
+            raise ValueError("ranmar: need n >= 1 and block length >= 1")
+        return out
+
+    def parse_jump_count(self, text: str) -> int:
+        limbs = np.zeros(4, np.uint64)
+        rc = self.lib.or_j256_parse(text.encode(), _p(limbs))
+        if rc != 0:
+            raise ValueError(f"ranmar: bad jump count {text!r}")
+        return sum(int(limbs[k]) << (64 * k) for k in range(4))
+
+    # -- workloads ----------------------------------------------------------
+    def generate_u32(self, states: np.ndarray, per_stream: int) -> np.ndarray:
+        states = np.ascontiguousarray(states)
+        out = np.empty(len(states) * per_stream, np.uint32)
+        self.lib.or_generate_u32(_p(states), len(states), per_stream, _p(out))
+        return out
+
+    def generate_f32(self, states: np.ndarray, per_stream: int) -> np.ndarray:
+        states = np.ascontiguousarray(states)
+        out = np.empty(len(states) * per_stream, np.float32)
+        self.lib.or_generate_f32(_p(states), len(states), per_stream, _p(out))
+        return out
+
+    def consume(self, states: np.ndarray, per_stream: int):
+        states = np.ascontiguousarray(states)
+        sums = np.empty(len(states), np.uint64)
+        hist = np.empty((len(states), 256), np.uint32)
+        self.lib.or_consume(_p(states), len(states), per_stream, _p(sums), _p(hist))
+        return sums, hist
+
+    def gaussian_fill(self, gstates: np.ndarray, per_step: int, steps: int) -> np.ndarray:
+        gstates = np.ascontiguousarray(gstates)
+        out = np.empty((steps, len(gstates), per_step), np.float64)
+        self.lib.or_gaussian_fill(_p(gstates), len(gstates), per_step, steps, _p(out))
+        return out
+
+    def to_text(self, state: np.ndarray) -> str:
+        buf = C.create_string_buffer(4096)
+        n = self.lib.or_to_text(_p(np.ascontiguousarray(state)), buf, 4096)
+        assert n > 0
+        return buf.value.decode()
+
+    def from_text(self, text: str) -> np.ndarray:
+        out = np.zeros(1, STATE_DTYPE)
+        if self.lib.or_from_text(text.encode(), _p(out)) != 0:
+            raise ValueError("ranmar: state parse error")
+        return out
+
+
+class Reference:
+    """The reference's own headers compiled in place (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing; {_build_hint()} with /root/reference present")
+        self.lib = C.CDLL(path)
+        L = self.lib
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        sig = {
+            "ref_init": (i32, [u32, vp]),
+            "ref_step_n": (i32, [vp, u64, vp]),
+            "ref_step_float_n": (i32, [u32, u64, vp]),
+            "ref_pow_t_mod": (i32, [vp, vp]),
+            "ref_mul_mod": (i32, [vp, vp, vp]),
+            "ref_jump_state": (i32, [vp, vp, vp]),
+            "ref_jump_arith": (i32, [u32, vp, vp]),
+            "ref_make_streams": (i32, [u32, vp, u64, i32, vp]),
+            "ref_parse_jump_count": (i32, [C.c_char_p, vp]),
+            "ref_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
+            "ref_from_text": (i32, [C.c_char_p, vp]),
+            "ref_generate_f32": (i32, [vp, vp, u64, u64, u64, i32, vp, vp]),
+            "ref_stream_starts": (i32, [vp, vp, u64, u64, i32, vp]),
+            "ref_jump_batch": (i32, [vp, u64, vp, i32, vp]),
+            "ref_consume": (i32, [vp, vp, u64, u64, u64, i32, vp, vp]),
+            "ref_last_error": (C.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+
+    def _check(self, rc: int):
+        if rc == 1:
+            raise ValueError(self.lib.ref_last_error().decode())
+        if rc != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def init(self, seed: int) -> np.ndarray:
+        s = np.zeros(1, STATE_DTYPE)
+        self._check(self.lib.ref_init(seed, _p(s)))
+        return s
+
+    def step_n(self, state: np.ndarray, n: int) -> np.ndarray:
+        out = np.empty(n, np.uint32)
+        self.lib.ref_step_n(_p(state), n, _p(out))
+        return out
+
+    def float_outputs(self, seed: int, n: int) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        self._check(self.lib.ref_step_float_n(seed, n, _p(out)))
+        return out
+
+    def pow_t_mod(self, j: int) -> np.ndarray:
+        out = np.empty(97, np.uint32)
+        self._check(self.lib.ref_pow_t_mod(_p(j_limbs(j)), _p(out)))
+        return out
+
+    def mul_mod(self, a, b) -> np.ndarray:
+        out = np.empty(97, np.uint32)
+        self.lib.ref_mul_mod(_p(np.ascontiguousarray(a, np.uint32)),
+                             _p(np.ascontiguousarray(b, np.uint32)), _p(out))
+        return out
+
+    def jump_state(self, state: np.ndarray, j: int) -> np.ndarray:
+        out = np.zeros(1, STATE_DTYPE)
+        self._check(self.lib.ref_jump_state(_p(np.ascontiguousarray(state)), _p(j_limbs(j)),
+                                             _p(out)))
+        return out
+
+    def make_streams(self, seed: int, j: int, n: int, independent: bool = False) -> np.ndarray:
+        out = np.zeros(n, STATE_DTYPE)
+        self._check(self.lib.ref_make_streams(seed, _p(j_limbs(j)), n, int(independent), _p(out)))
+        return out
+
+    def stream_starts(self, base: np.ndarray, j: int, first: int, n: int,
+                      threads: int = 1) -> np.ndarray:
+        out = np.zeros(n, STATE_DTYPE)
+        self._check(self.lib.ref_stream_starts(_p(np.ascontiguousarray(base)), _p(j_limbs(j)),
+                                               first, n, threads, _p(out)))
+        return out
+
+    def jump_batch(self, states: np.ndarray, j: int, threads: int = 1) -> np.ndarray:
+        states = np.ascontiguousarray(states)
+        out = np.zeros(len(states), STATE_DTYPE)
+        self._check(self.lib.ref_jump_batch(_p(states), len(states), _p(j_limbs(j)), threads,
+                                            _p(out)))
+        return out
+
+    def generate_f32(self, base: np.ndarray, j: int, first: int, n: int, per_stream: int,
+                     threads: int = 1, out: np.ndarray | None = None) -> int:
+        chk = np.zeros(1, np.uint64)
+        self._check(self.lib.ref_generate_f32(
+            _p(np.ascontiguousarray(base)), _p(j_limbs(j)), first, n, per_stream, threads,
+            _p(out) if out is not None else None, _p(chk)))
+        return int(chk[0])
+
+    def consume(self, base: np.ndarray, j: int, first: int, n: int, per_stream: int,
+                threads: int = 1):
+        sums = np.empty(n, np.uint64)
+        hist = np.empty((n, 256), np.uint32)
+        self._check(self.lib.ref_consume(_p(np.ascontiguousarray(base)), _p(j_limbs(j)), first, n,
+                                         per_stream, threads, _p(sums), _p(hist)))
+        return sums, hist
+
+    def parse_jump_count(self, text: str) -> int:
+        limbs = np.zeros(4, np.uint64)
+        self._check(self.lib.ref_parse_jump_count(text.encode(), _p(limbs)))
+        return sum(int(limbs[k]) << (64 * k) for k in range(4))
+
+    def to_text(self, state: np.ndarray) -> str:
+        buf = C.create_string_buffer(4096)
+        n = self.lib.ref_to_text(_p(np.ascontiguousarray(state)), buf, 4096)
+        assert n > 0
+        return buf.value.decode()
+
+    def from_text(self, text: str) -> np.ndarray:
+        out = np.zeros(1, STATE_DTYPE)
+        self._check(self.lib.ref_from_text(text.encode(), _p(out)))
+        return out
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
