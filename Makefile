@@ -1,0 +1,41 @@
+# Builds the product library (sm_100a) and the test-only oracle.
+#   make            -> paper_2512_00093_b200/lib/libranmar_b200.so + oracle
+#   make sass       -> SASS dump of the kernels (profiles/ evidence)
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -Xptxas -warn-spills
+PKG := paper_2512_00093_b200
+CSRC := $(PKG)/csrc
+BUILD := $(PKG)/build
+LIB := $(PKG)/lib/libranmar_b200.so
+OBJS := $(BUILD)/gen_kernels.o $(BUILD)/jump_kernels.o $(BUILD)/ranmar_abi.o
+HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh
+
+.PHONY: all lib oracle ref clean sass
+all: lib oracle
+
+lib: $(LIB)
+
+$(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; exit 1)
+
+$(BUILD)/ranmar_abi.o: $(CSRC)/ranmar_abi.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(BUILD)/kernels.sass
+
+clean:
+	rm -rf $(BUILD) $(PKG)/lib

@@ -1,0 +1,435 @@
+"""Benchmark: B200 RANMAR generation + exact jump-ahead (arXiv 2512.00093).
+
+Headline (BASELINE.json metric "RANMAR uniforms/s & HBM GB/s"): config 2 —
+65,536 streams of make_streams(12345, 2^40) x 65,536 fp32 uniforms each
+(2^32 values, 16 GiB stored to HBM). One step = the GPU's whole job for that
+config: the stream starts (K3, make_streams) and the stored uniforms (K1).
+At N GPUs each rank does the same job for its own stream range
+[rank * 65536, (rank + 1) * 65536) of the same sequence (weak scaling, no
+collective on the data path); NCCL only gathers per-rank checksums afterwards.
+
+Extra keys on the same JSON line: config 3 (2^20 stream starts at J=2^120,
+jumps/s), config 4 (consume-in-kernel, uniforms/s), config 5 (gaussians).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(seed=12345, j=2**40, n=65536, per=65536)
+C3 = dict(seed=987654321, j=2**120, n=1 << 20)
+C4 = dict(seed=42, j=2**64, n=1 << 20, per=1 << 20)
+C5 = dict(seed=7, j=2**50, n=1 << 24, per=3, steps=100)
+METRIC = "RANMAR uniforms/s & HBM GB/s at 1/2/4/8 B200; jump-aheads/s at J=2^120"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_checksums(sums, world: int):
+    """NCCL all-gather of per-rank checksums (after the timed region only)."""
+    import torch
+    if world == 1:
+        return [sums]
+    import torch.distributed as dist
+    t = torch.tensor(sums, dtype=torch.int64, device="cuda")
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
+
+
+def load_traffic(kernel_key: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(kernel_key)
+    return None
+
+
+# ------------------------------------------------------------------ CPU arms
+
+def cpu_reference_c2(steps: int = 1, threads: int | None = None):
+    """The reference's own code (oracle/_ref, headers compiled in place) on the
+    host cores, on a bounded sample of config 2. Returns a dict or None."""
+    from oracle.bind import Reference, reference_available
+    threads = threads or os.cpu_count() or 1
+    n = int(min(C2["n"], 16384, 64 * threads))
+    out = np.empty(n * C2["per"], np.float32)
+    if reference_available():
+        ref, kind = Reference(), "reference"
+        base = ref.init(C2["seed"])
+        run = lambda: ref.generate_f32(base, C2["j"], 0, n, C2["per"], threads, out)  # noqa: E731
+    else:  # fall back to the C restatement (single-threaded port)
+        from oracle.bind import Oracle
+        orc, kind, threads = Oracle(), "port", 1
+        n = 256
+        out = np.empty(n * C2["per"], np.float32)
+
+        def run():
+            ss = orc.make_streams(orc.init(C2["seed"]), C2["j"], n)
+            out[:] = orc.generate_f32(ss, C2["per"])
+    run()  # warm-up (page-faults the output buffer)
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": n * C2["per"] / t, "unit": "uniforms/s", "cores": threads, "kind": kind,
+            "sample": f"config 2 streams [0, {n}) x {C2['per']} fp32 (make_streams + step, "
+                      f"stored to host RAM), {threads} threads, median of {len(times)}",
+            "seconds": t}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    cb = cpu_reference_c2(steps=args.steps)
+    line = {"metric": METRIC, "impl": "reference", "value": cb["value"], "unit": "uniforms/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, BASELINE config 2)",
+            "config": {"workload": "config 2 sample: make_streams(12345, 2^40) x 65536 fp32 per stream",
+                       "streams": cb["sample"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "uniforms/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_2512_00093_b200 as rb
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    peak, peak_kind = measured_peaks()
+    extras = {}
+
+    # ---- config 2: make_streams + 2^32 fp32 stored, per rank ----
+    n, per = C2["n"], C2["per"]
+    first = rank * n
+    base = rb.init(C2["seed"])
+    states = torch.empty((n, rb.STATE_WORDS), dtype=torch.int32, device=dev)
+    ws = torch.empty(rb.lib().ranmar_make_streams_workspace(n), dtype=torch.uint8, device=dev)
+    out = torch.empty(n * per, dtype=torch.float32, device=dev)
+
+    def step(ev=None):
+        with torch.cuda.stream(stream):
+            rb.make_streams_dev(base, C2["j"], n, first=first, out=states, workspace=ws,
+                                stream=stream)
+            if ev:
+                ev[0].record(stream)
+            rb.generate(states, per, "f32", out=out, stream=stream)
+            if ev:
+                ev[1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    gen_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = rb.kernel_launches()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            step(gen_events[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = rb.kernel_launches() - launches0
+    ms_local = t0.elapsed_time(t1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    gen_ms = statistics.mean(a.elapsed_time(b) for a, b in gen_events)
+    uniforms_step = n * per * world
+    value = uniforms_step / (ms * 1e-3)
+    gen_bytes = n * per * 4
+    achieved = gen_bytes / (gen_ms * 1e-3) / 1e9
+    # checksum of this rank's last step, gathered over NCCL after timing
+    with torch.cuda.stream(stream):
+        chk = int((out.view(n, per)[:, :1024].double() * 2**24).sum().item())
+    sums = gather_checksums([chk, first], world)
+
+    # ---- e2e: the same job through the host-buffer C-ABI path ----
+    e2e = None
+    if not args.no_e2e:
+        ctx = rb.Context(local)
+        host_states = np.zeros(n, rb.STATE_DTYPE)
+        host_out = torch.empty(n * per, dtype=torch.float32, pin_memory=True).numpy()
+        e2e_steps = max(1, min(args.steps, 3))
+        ctx.make_streams(C2["seed"], C2["j"], n, first=first, out=host_states)
+        ctx.generate(host_states, per, "f32", out=host_out)  # warm-up
+        h2d = d2h = 0
+        barrier(world)
+        tt = time.perf_counter()
+        for _ in range(e2e_steps):
+            ctx.make_streams(C2["seed"], C2["j"], n, first=first, out=host_states)
+            a, b = ctx.traffic()
+            ctx.generate(host_states, per, "f32", out=host_out)
+            c, d = ctx.traffic()
+            h2d, d2h = a + c, b + d
+        e2e_s = max_over_ranks((time.perf_counter() - tt) / e2e_steps, world)
+        # host result equals the device result of the timed step
+        assert np.array_equal(host_out[:per * 4], out[:per * 4].cpu().numpy())
+        e2e = {"value": uniforms_step / e2e_s, "unit": "uniforms/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+               "path": "ranmar_ctx_make_streams + ranmar_ctx_generate_f32 into pinned host memory"}
+        del host_out
+        ctx.close()
+
+    # ---- config 3: 2^20 stream starts at J = 2^120 (jump-aheads/s) ----
+    if not args.quick:
+        n3 = C3["n"]
+        base3 = rb.init_unchecked(C3["seed"])
+        st3 = torch.empty((n3, rb.STATE_WORDS), dtype=torch.int32, device=dev)
+        ws3 = torch.empty(rb.lib().ranmar_make_streams_workspace(n3), dtype=torch.uint8, device=dev)
+        first3 = rank * n3
+
+        def step3():
+            rb.make_streams_dev(base3, C3["j"], n3, first=first3, out=st3, workspace=ws3,
+                                stream=stream)
+
+        for _ in range(3):
+            step3()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        reps = 10
+        for _ in range(reps):
+            step3()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms3 = max_over_ranks(a.elapsed_time(b) / reps, world)
+        # generic batched jump: every state jumped by 2^120 (one P_J, 2^20 applies)
+        jo = torch.empty_like(st3)
+        rb.jump_dev(st3, C3["j"], out=jo, stream=stream)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            rb.jump_dev(st3, C3["j"], out=jo, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        msj = max_over_ranks(a.elapsed_time(b) / reps, world)
+        extras["config3"] = {
+            "workload": "make_streams(init_unchecked(987654321), 2^120): 2^20 stream starts s_{kJ} per rank",
+            "jump_aheads_per_s": n3 * world / (ms3 * 1e-3), "ms": ms3,
+            "batched_jump_state_per_s": n3 * world / (msj * 1e-3), "batched_jump_ms": msj,
+            "macs_per_start": 2 * 97 * 97}
+        del st3, ws3, jo
+
+    # ---- config 4: consume in kernel (no store) ----
+    if not args.quick:
+        n4 = C4["n"] if not args.c4_streams else args.c4_streams
+        st4 = torch.empty((n4, rb.STATE_WORDS), dtype=torch.int32, device=dev)
+        ws4 = torch.empty(rb.lib().ranmar_make_streams_workspace(n4), dtype=torch.uint8, device=dev)
+        sums4 = torch.empty(n4, dtype=torch.int64, device=dev)
+        hist4 = torch.empty((n4, 256), dtype=torch.int32, device=dev)
+        first4 = rank * n4
+
+        def step4():
+            rb.make_streams_dev(rb.init(C4["seed"]), C4["j"], n4, first=first4, out=st4,
+                                workspace=ws4, stream=stream)
+            rb.consume(st4, C4["per"], sums=sums4, hist=hist4, stream=stream)
+
+        step4()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step4()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms4 = max_over_ranks(a.elapsed_time(b), world)
+        extras["config4"] = {"workload": f"{n4} streams x 2^20 uniforms consumed per rank "
+                                         "(make_streams(42, 2^64) + per-stream u64 sum + 256-bin hist)",
+                             "uniforms_per_s": n4 * C4["per"] * world / (ms4 * 1e-3), "ms": ms4}
+        del st4, ws4, sums4, hist4
+
+    # ---- config 5: gaussians ----
+    if not args.quick:
+        n5 = C5["n"]
+        st5 = torch.empty((n5, rb.STATE_WORDS), dtype=torch.int32, device=dev)
+        ws5 = torch.empty(rb.lib().ranmar_make_streams_workspace(n5), dtype=torch.uint8, device=dev)
+        rb.make_streams_dev(rb.init(C5["seed"]), C5["j"], n5, first=rank * n5, out=st5,
+                            workspace=ws5, stream=stream)
+        g5 = rb.gauss_states_from(st5)
+        del st5, ws5
+        out5 = torch.empty((C5["steps"], n5, C5["per"]), dtype=torch.float64, device=dev)
+        g5w = g5.clone()
+        rb.gaussian(g5w, C5["per"], 2, out=out5[:2], stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        g5w.copy_(g5)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rb.gaussian(g5w, C5["per"], C5["steps"], out=out5, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms5 = max_over_ranks(a.elapsed_time(b), world)
+        nbytes = out5.numel() * 8 + 2 * n5 * 416
+        extras["config5"] = {"workload": "2^24 atoms x 3 gaussian() x 100 steps per rank, fp64 out",
+                             "gaussians_per_s": out5.numel() * world / (ms5 * 1e-3), "ms": ms5,
+                             "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9}
+        del out5, g5, g5w
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cb = cpu_reference_c2(steps=1)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {
+        "metric": METRIC, "value": value, "unit": "uniforms/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded streams, BASELINE config 2)",
+        "config": {"workload": "config 2: make_streams(12345, 2^40) streams [rank*65536, +65536) "
+                               "x 65536 fp32 uniforms stored per rank (16 GiB/rank)",
+                   "streams_per_rank": n, "per_stream": per, "output": "fp32, stream-major",
+                   "l2": "output (16 GiB) >> L2 (126 MB): no flush needed",
+                   "parallelism": f"stream-range partition x{world}, no data-path collective"},
+        "hbm_GB_per_s": n * per * 4 * world / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "gen_store_kernel<float>", "achieved": achieved,
+                     "peak": peak, "peak_kind": f"{peak_kind} copy GB/s (MEASURED_PEAKS.json hbm_gbs)",
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": load_traffic("gen_store_kernel<float>"),
+                     "algorithmic_bytes_per_launch": gen_bytes, "kernel_ms": gen_ms},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        "checksums": sums, **extras,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--quick", action="store_true", help="config 2 only")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--c4-streams", type=int, default=0)
+    args = ap.parse_args()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/* ranmar_b200.h — C ABI of the B200-native RANMAR generator + exact jump-ahead.
+ *
+ * Drop-in boundary for the reference library ranmar24
+ * (/root/reference/proj/include/ranmar, header-only C++20, arXiv 2512.00093).
+ * Every entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj). Plain C types only: no torch, no C++.
+ *
+ * Conventions
+ *  - Return value: RANMAR_OK (0) or a RANMAR_E* code; ranmar_last_error()
+ *    gives a thread-local message. RANMAR_EINVAL is returned exactly where
+ *    the reference throws std::invalid_argument (SURVEY §8b "Errors").
+ *  - "_dev" functions take device pointers and a cudaStream_t passed as
+ *    void*; they are asynchronous and stream-ordered, allocate nothing, and
+ *    run hand-written sm_100a kernels. There is no CPU fallback: without a
+ *    usable CUDA device they return RANMAR_ECUDA.
+ *  - "ranmar_ctx_*" functions take HOST buffers and do the host<->device
+ *    copies themselves (pinned/pageable both accepted), synchronously.
+ *  - Stream-major output layout: out[k * per_stream + n] is output n (0-based)
+ *    of stream k.
+ */
+#ifndef RANMAR_B200_H
+#define RANMAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RANMAR_ABI_VERSION 1
+
+enum {
+    RANMAR_OK = 0,
+    RANMAR_EINVAL = 1, /* the reference throws std::invalid_argument here */
+    RANMAR_ERANGE = 2, /* jump count or size outside what the ABI represents */
+    RANMAR_ECUDA = 3,  /* CUDA runtime/launch failure or no device */
+    RANMAR_ESTATE = 4, /* a device state violated the invariants (see ranmar_device_status) */
+    RANMAR_ENOMEM = 5  /* workspace too small / allocation failed */
+};
+
+/* ranmar::RanmarState (core.hpp:29-49), byte-identical: 97 lanes < 2^24 in a
+ * ring, 0-based cursors i, j with (i - j) mod 97 == 64, arithmetic residue
+ * v < 2^24 - 3. sizeof == 400. */
+typedef struct ranmar_state {
+    uint32_t lane[97];
+    int32_t i;
+    int32_t j;
+    uint32_t v;
+} ranmar_state;
+
+/* ranmar::JumpCount (jumpcount.hpp:13, an unbounded cpp_int) as 256-bit
+ * little-endian limbs; the generator's period is ~2^144. */
+typedef struct ranmar_jump_count {
+    uint64_t limb[4];
+} ranmar_jump_count;
+
+/* State + the cached second polar deviate of gaussian() (416 B). */
+typedef struct ranmar_gauss_state {
+    ranmar_state s;
+    double saved;
+    uint32_t has_saved;
+    uint32_t pad;
+} ranmar_gauss_state;
+
+typedef struct ranmar_ctx ranmar_ctx;
+
+/* ------------------------------------------------------------ host, no GPU */
+int ranmar_abi_version(void);
+const char* ranmar_last_error(void);
+
+/* ranmar::init(seed)             init.hpp:18-51 (EINVAL if seed > 900000000, :19-20) */
+int ranmar_init(uint32_t seed, ranmar_state* out);
+/* Same seed expansion without the range check (BASELINE config 3 uses seed
+ * 987654321, which ranmar::init rejects; documented deviation). */
+int ranmar_init_unchecked(uint32_t seed, ranmar_state* out);
+/* ranmar::value_of(u24)          core.hpp:75-79 (EINVAL if u24 > 2^24-1) */
+int ranmar_value_of(uint32_t u24, double* out);
+/* ranmar::parse_jump_count(text) jumpcount.hpp:16-47 (EINVAL on bad text;
+ * ERANGE if the value does not fit 256 bits) */
+int ranmar_parse_jump_count(const char* text, ranmar_jump_count* out);
+/* ranmar::jump_arith(a, J).v     jump.hpp:79-86 (closed form, host) */
+int ranmar_jump_arith(uint32_t v, const ranmar_jump_count* j, uint32_t* out);
+/* ranmar::to_text / from_text    serialize.hpp:21-40 / :81-136. to_text
+ * returns the length written (cap must hold it + NUL) or -1. */
+long ranmar_to_text(const ranmar_state* s, char* buf, long cap);
+int ranmar_from_text(const char* text, ranmar_state* out);
+
+/* -------------------------------------------------- device ops (async) --- */
+
+/* Workspace bytes needed by ranmar_make_streams_dev / ranmar_jump_dev for n
+ * streams. */
+size_t ranmar_make_streams_workspace(uint64_t n);
+
+/* Streams [first, first + n) of ranmar::make_streams(base, J, ·)
+ * (jump.hpp:108-124): stream k starts at s_{kJ} of `base` (a HOST state).
+ * Stream 0 is `base` itself, like make_streams' streams.front(); every other
+ * stream is in jump_state's normalised layout (jump.hpp:42-48). Both
+ * StreamModes give these states (test_jump.cpp:191-196). EINVAL if n == 0 or
+ * J == 0 (jump.hpp:111-112). first + n must be < 2^63. */
+int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j, uint64_t first,
+                            uint64_t n, ranmar_state* d_out, void* d_workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* d_out[k] = ranmar::jump_state(d_in[k], J) for k < n (jump.hpp:90-95).
+ * d_in == d_out is allowed. */
+int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
+                    const ranmar_jump_count* j, void* d_workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ranmar::poly::pow_t_mod<24>(J) (polyring.hpp:113-124) into d_coeff[97]. */
+int ranmar_pow_t_mod_dev(const ranmar_jump_count* j, uint32_t* d_coeff, void* stream);
+
+/* per_stream calls of ranmar::step (core.hpp:54-66) on each of n_streams
+ * device states, advancing them in place exactly as step() would (ring
+ * contents and cursors included). Outputs: u24 in u32, next_f64 narrowed to
+ * f32 (exact), or next_f64 (core.hpp:70-72). */
+int ranmar_generate_u32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            uint32_t* d_out, void* stream);
+int ranmar_generate_f32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            float* d_out, void* stream);
+int ranmar_generate_f64_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            double* d_out, void* stream);
+
+/* Consume-in-kernel (no uniform is stored): per stream, the u64 sum of its
+ * per_stream 24-bit outputs and a 256-bin histogram of (u >> 16);
+ * d_hist is n_streams x 256 u32. States advance in place. */
+int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                       uint64_t* d_sums, uint32_t* d_hist, void* stream);
+
+/* gaussian() (no reference counterpart; Marsaglia polar, NR gasdev pairing):
+ * for each atom, steps x per_step calls; d_out[(step * n_atoms + atom) *
+ * per_step + c]. States (and the cached deviate) advance in place. */
+int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
+                            uint64_t steps, double* d_out, void* stream);
+
+/* Sticky status bits of the current device (bit 0: a kernel met a state with
+ * bad cursors / v >= m). Synchronises the device. clear != 0 resets them. */
+int ranmar_device_status(uint32_t* flags, int clear);
+
+/* Number of kernels this library has launched in this process (all devices);
+ * diagnostic evidence for benchmarks ("gpu_launches"). */
+uint64_t ranmar_kernel_launches(void);
+
+/* ------------------------------------------- host-buffer ops (sync, e2e) --- */
+int ranmar_ctx_create(int device, ranmar_ctx** out);
+void ranmar_ctx_destroy(ranmar_ctx* ctx);
+/* ranmar::make_streams(seed, J, n) (jump.hpp:108-124) -> h_out[n]. */
+int ranmar_ctx_make_streams(ranmar_ctx* ctx, uint32_t seed, const ranmar_jump_count* j,
+                            uint64_t first, uint64_t n, ranmar_state* h_out);
+/* ranmar::jump_state on host arrays. */
+int ranmar_ctx_jump(ranmar_ctx* ctx, const ranmar_state* h_in, ranmar_state* h_out, uint64_t n,
+                    const ranmar_jump_count* j);
+/* Generation into host memory, pipelined in chunks (copy-out overlapped with
+ * generation). h_states advance in place. */
+int ranmar_ctx_generate_u32(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n_streams,
+                            uint64_t per_stream, uint32_t* h_out);
+int ranmar_ctx_generate_f32(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n_streams,
+                            uint64_t per_stream, float* h_out);
+int ranmar_ctx_consume(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n_streams,
+                       uint64_t per_stream, uint64_t* h_sums, uint32_t* h_hist);
+/* Bytes moved host->device and device->host by the last ctx call. */
+int ranmar_ctx_last_traffic(ranmar_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANMAR_B200_H */

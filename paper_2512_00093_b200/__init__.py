@@ -1,0 +1,392 @@
+"""B200-native RANMAR (arXiv 2512.00093) behind the reference's interface.
+
+Python mirror of the reference library's API (/root/reference/proj/include/
+ranmar, namespace ``ranmar``) over the C ABI in ``include/ranmar_b200.h``
+(``lib/libranmar_b200.so``, sm_100a kernels). Same names, same argument
+meaning, and ``ValueError`` wherever the reference throws
+``std::invalid_argument``. Device buffers are torch CUDA tensors; torch is
+only plumbing (allocation, streams), never the compute path.
+
+There is no CPU fallback: the generation / jump entry points need the built
+library and a CUDA device and raise ``RuntimeError`` otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libranmar_b200.so")
+
+# ranmar::RanmarState (core.hpp:29-49) == ranmar_state: 400 bytes.
+STATE_DTYPE = np.dtype([("lane", "<u4", (97,)), ("i", "<i4"), ("j", "<i4"), ("v", "<u4")])
+GAUSS_DTYPE = np.dtype([("s", STATE_DTYPE), ("saved", "<f8"), ("has_saved", "<u4"), ("pad", "<u4")])
+STATE_WORDS = 100
+GAUSS_WORDS = 104
+
+long_lag, short_lag, word_bits = 97, 33, 24             # core.hpp:17-19
+word_mask = 0x00FFFFFF                                  # core.hpp:20
+arith_mod, arith_delta, arith_start = 16777213, 7654321, 362436  # core.hpp:22-24
+max_seed = 900000000                                    # init.hpp:16
+
+OK, EINVAL, ERANGE, ECUDA, ESTATE, ENOMEM = range(6)
+
+
+class StreamMode(enum.Enum):
+    """jump.hpp:101-104. Both modes produce identical states."""
+    incremental = 0
+    independent = 1
+
+
+class RanmarError(RuntimeError):
+    pass
+
+
+class _JumpCount(C.Structure):
+    _fields_ = [("limb", C.c_uint64 * 4)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads the CUDA library (fails loudly if it was never built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `make lib` "
+                           f"(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, u32, u64, i32, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_size_t
+    jp = C.POINTER(_JumpCount)
+    sig = {
+        "ranmar_abi_version": (i32, []),
+        "ranmar_last_error": (C.c_char_p, []),
+        "ranmar_init": (i32, [u32, vp]),
+        "ranmar_init_unchecked": (i32, [u32, vp]),
+        "ranmar_value_of": (i32, [u32, C.POINTER(C.c_double)]),
+        "ranmar_parse_jump_count": (i32, [C.c_char_p, jp]),
+        "ranmar_jump_arith": (i32, [u32, jp, C.POINTER(C.c_uint32)]),
+        "ranmar_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
+        "ranmar_from_text": (i32, [C.c_char_p, vp]),
+        "ranmar_make_streams_workspace": (sz, [u64]),
+        "ranmar_make_streams_dev": (i32, [vp, jp, u64, u64, vp, vp, sz, vp]),
+        "ranmar_jump_dev": (i32, [vp, vp, u64, jp, vp, sz, vp]),
+        "ranmar_pow_t_mod_dev": (i32, [jp, vp, vp]),
+        "ranmar_generate_u32_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_generate_f32_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_generate_f64_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
+        "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
+        "ranmar_device_status": (i32, [C.POINTER(C.c_uint32), i32]),
+        "ranmar_kernel_launches": (u64, []),
+        "ranmar_ctx_create": (i32, [i32, C.POINTER(vp)]),
+        "ranmar_ctx_destroy": (None, [vp]),
+        "ranmar_ctx_make_streams": (i32, [vp, u32, jp, u64, u64, vp]),
+        "ranmar_ctx_jump": (i32, [vp, vp, vp, u64, jp]),
+        "ranmar_ctx_generate_u32": (i32, [vp, vp, u64, u64, vp]),
+        "ranmar_ctx_generate_f32": (i32, [vp, vp, u64, u64, vp]),
+        "ranmar_ctx_consume": (i32, [vp, vp, u64, u64, vp, vp]),
+        "ranmar_ctx_last_traffic": (i32, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc == OK:
+        return
+    msg = lib().ranmar_last_error().decode()
+    if rc == EINVAL:
+        raise ValueError(msg)
+    raise RanmarError(f"[{rc}] {msg}")
+
+
+def _jc(j) -> _JumpCount:
+    """int (or text accepted by parse_jump_count) -> C jump count."""
+    if isinstance(j, str):
+        j = parse_jump_count(j)
+    j = int(j)
+    if j < 0:
+        raise ValueError("ranmar: jump count must be nonnegative")  # polyring.hpp:115-116
+    if j >= 1 << 256:
+        raise RanmarError("ranmar: jump count exceeds 2^256 - 1")
+    out = _JumpCount()
+    for k in range(4):
+        out.limb[k] = (j >> (64 * k)) & ((1 << 64) - 1)
+    return out
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ----------------------------------------------------------------- host side
+
+def init(seed: int) -> np.ndarray:
+    """ranmar::init (init.hpp:18-51). Returns a 1-element STATE_DTYPE array."""
+    if not 0 <= seed < 1 << 32:
+        raise ValueError("ranmar: seed must be in [0, 900000000]")
+    s = np.zeros(1, STATE_DTYPE)
+    _check(lib().ranmar_init(seed, _ptr(s)))
+    return s
+
+
+def init_unchecked(seed: int) -> np.ndarray:
+    """Seed expansion without init()'s range check (BASELINE config 3's seed)."""
+    s = np.zeros(1, STATE_DTYPE)
+    _check(lib().ranmar_init_unchecked(seed, _ptr(s)))
+    return s
+
+
+def value_of(u24: int) -> float:
+    """ranmar::value_of (core.hpp:75-79)."""
+    out = C.c_double()
+    _check(lib().ranmar_value_of(u24, C.byref(out)))
+    return out.value
+
+
+def parse_jump_count(text: str) -> int:
+    """ranmar::parse_jump_count (jumpcount.hpp:16-47)."""
+    j = _JumpCount()
+    _check(lib().ranmar_parse_jump_count(text.encode(), C.byref(j)))
+    return sum(int(j.limb[k]) << (64 * k) for k in range(4))
+
+
+def jump_arith(v: int, j) -> int:
+    """ranmar::jump_arith(ArithState{v}, J).v (jump.hpp:79-86)."""
+    out = C.c_uint32()
+    jc = _jc(j)
+    _check(lib().ranmar_jump_arith(v, C.byref(jc), C.byref(out)))
+    return out.value
+
+
+def to_text(state: np.ndarray) -> str:
+    """ranmar::to_text (serialize.hpp:21-40)."""
+    buf = C.create_string_buffer(4096)
+    n = lib().ranmar_to_text(_ptr(np.ascontiguousarray(state, STATE_DTYPE)), buf, 4096)
+    if n < 0:
+        raise RanmarError("to_text buffer too small")
+    return buf.value.decode()
+
+
+def from_text(text: str) -> np.ndarray:
+    """ranmar::from_text (serialize.hpp:81-136)."""
+    s = np.zeros(1, STATE_DTYPE)
+    _check(lib().ranmar_from_text(text.encode(), _ptr(s)))
+    return s
+
+
+# ---------------------------------------------------------------- device side
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RanmarError("no CUDA device: the B200 kernels are the only implementation")
+    return torch
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def states_to_device(states: np.ndarray, device="cuda"):
+    """STATE_DTYPE array -> int32 CUDA tensor [n, 100] (same bytes)."""
+    torch = _torch()
+    a = np.ascontiguousarray(states, STATE_DTYPE).view(np.int32).reshape(-1, STATE_WORDS)
+    return torch.from_numpy(a.copy()).to(device)
+
+
+def states_to_host(t) -> np.ndarray:
+    """int32 CUDA tensor [n, 100] -> STATE_DTYPE array."""
+    return t.detach().cpu().contiguous().numpy().view(STATE_DTYPE).reshape(-1)
+
+
+def _dptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def make_streams_dev(base: np.ndarray, j, n: int, first: int = 0, out=None, workspace=None,
+                     stream=None):
+    """Streams [first, first+n) of make_streams(base, J) (jump.hpp:108-124) on the GPU.
+    Returns an int32 CUDA tensor [n, 100] of ranmar_state records."""
+    torch = _torch()
+    if n == 0:
+        raise ValueError("ranmar: need at least one stream")
+    jc = _jc(j)
+    if out is None:
+        out = torch.empty((n, STATE_WORDS), dtype=torch.int32, device="cuda")
+    wsb = lib().ranmar_make_streams_workspace(n)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    b = np.ascontiguousarray(base, STATE_DTYPE).reshape(-1)[:1]
+    _check(lib().ranmar_make_streams_dev(_ptr(b), C.byref(jc), first, n, _dptr(out),
+                                         _dptr(workspace), workspace.numel(), _stream_ptr(stream)))
+    return out
+
+
+def make_streams(seed: int, block_length, n_streams: int,
+                 mode: StreamMode = StreamMode.incremental, first: int = 0):
+    """ranmar::make_streams(seed, J, n, mode) (jump.hpp:108-124), computed on the GPU.
+    Returns a CUDA tensor of states; `mode` does not change the result."""
+    if n_streams == 0:
+        raise ValueError("ranmar: need at least one stream")
+    if int(block_length) < 1:
+        raise ValueError("ranmar: block length must be >= 1")
+    return make_streams_dev(init(seed), block_length, n_streams, first=first)
+
+
+def jump_dev(states, j, out=None, stream=None):
+    """out[k] = jump_state(states[k], J) (jump.hpp:90-95)."""
+    torch = _torch()
+    jc = _jc(j)
+    n = states.shape[0]
+    if out is None:
+        out = torch.empty_like(states)
+    ws = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    _check(lib().ranmar_jump_dev(_dptr(states), _dptr(out), n, C.byref(jc), _dptr(ws), 4096,
+                                 _stream_ptr(stream)))
+    return out
+
+
+def jump_state(state: np.ndarray, j) -> np.ndarray:
+    """ranmar::jump_state on one host state, computed on the GPU."""
+    return states_to_host(jump_dev(states_to_device(state), j))
+
+
+def pow_t_mod_dev(j, stream=None):
+    """ranmar::poly::pow_t_mod<24>(J) (polyring.hpp:113-124) -> int32 CUDA tensor [97]."""
+    torch = _torch()
+    jc = _jc(j)
+    out = torch.empty(97, dtype=torch.int32, device="cuda")
+    _check(lib().ranmar_pow_t_mod_dev(C.byref(jc), _dptr(out), _stream_ptr(stream)))
+    return out
+
+
+_GEN = {"u32": ("ranmar_generate_u32_dev", "int32"), "f32": ("ranmar_generate_f32_dev", "float32"),
+        "f64": ("ranmar_generate_f64_dev", "float64")}
+
+
+def generate(states, per_stream: int, fmt: str = "f32", out=None, stream=None):
+    """per_stream x step() per stream (core.hpp:54-72), states advanced in place.
+    Returns the stream-major output [n * per_stream] (u32 outputs as int32)."""
+    torch = _torch()
+    fn, dt = _GEN[fmt]
+    n = states.shape[0]
+    if out is None:
+        out = torch.empty(n * per_stream, dtype=getattr(torch, dt), device="cuda")
+    _check(getattr(lib(), fn)(_dptr(states), n, per_stream, _dptr(out), _stream_ptr(stream)))
+    return out
+
+
+def consume(states, per_stream: int, sums=None, hist=None, stream=None):
+    """Per-stream u64 sum of the 24-bit outputs and 256-bin histogram of u >> 16."""
+    torch = _torch()
+    n = states.shape[0]
+    if sums is None:
+        sums = torch.empty(n, dtype=torch.int64, device="cuda")
+    if hist is None:
+        hist = torch.empty((n, 256), dtype=torch.int32, device="cuda")
+    _check(lib().ranmar_consume_dev(_dptr(states), n, per_stream, _dptr(sums), _dptr(hist),
+                                    _stream_ptr(stream)))
+    return sums, hist
+
+
+def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
+    """steps x per_step gaussian() calls per atom -> out[step, atom, c] (float64)."""
+    torch = _torch()
+    n = gstates.shape[0]
+    if out is None:
+        out = torch.empty((steps, n, per_step), dtype=torch.float64, device="cuda")
+    _check(lib().ranmar_gaussian_f64_dev(_dptr(gstates), n, per_step, steps, _dptr(out),
+                                         _stream_ptr(stream)))
+    return out
+
+
+def gauss_states_from(states_t):
+    """[n,100] state tensor -> [n,104] ranmar_gauss_state tensor with an empty cache."""
+    torch = _torch()
+    g = torch.zeros((states_t.shape[0], GAUSS_WORDS), dtype=torch.int32, device=states_t.device)
+    g[:, :STATE_WORDS] = states_t
+    return g
+
+
+def device_status(clear: bool = True) -> int:
+    """Sticky status bits of the current device (bit 0: a state with bad cursors or v)."""
+    flags = C.c_uint32()
+    _check(lib().ranmar_device_status(C.byref(flags), int(clear)))
+    return flags.value
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library so far in this process."""
+    return int(lib().ranmar_kernel_launches())
+
+
+class Context:
+    """Host-buffer API (ranmar_ctx_*): the call a CPU-side user of the reference
+    makes, with the host<->device copies inside."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().ranmar_ctx_create(device, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().ranmar_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def traffic(self) -> Tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(lib().ranmar_ctx_last_traffic(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def make_streams(self, seed: int, j, n: int, first: int = 0,
+                     out: Optional[np.ndarray] = None) -> np.ndarray:
+        jc = _jc(j)
+        if out is None:
+            out = np.zeros(n, STATE_DTYPE)
+        _check(lib().ranmar_ctx_make_streams(self._h, seed, C.byref(jc), first, n, _ptr(out)))
+        return out
+
+    def jump(self, states: np.ndarray, j) -> np.ndarray:
+        jc = _jc(j)
+        states = np.ascontiguousarray(states, STATE_DTYPE)
+        out = np.zeros(len(states), STATE_DTYPE)
+        _check(lib().ranmar_ctx_jump(self._h, _ptr(states), _ptr(out), len(states), C.byref(jc)))
+        return out
+
+    def generate(self, states: np.ndarray, per_stream: int, fmt: str = "f32",
+                 out: Optional[np.ndarray] = None) -> np.ndarray:
+        """states (STATE_DTYPE, advanced in place) -> host output."""
+        assert states.dtype == STATE_DTYPE and states.flags.c_contiguous
+        dt = {"f32": np.float32, "u32": np.uint32}[fmt]
+        if out is None:
+            out = np.empty(len(states) * per_stream, dt)
+        fn = lib().ranmar_ctx_generate_f32 if fmt == "f32" else lib().ranmar_ctx_generate_u32
+        _check(fn(self._h, _ptr(states), len(states), per_stream, _ptr(out)))
+        return out
+
+    def consume(self, states: np.ndarray, per_stream: int):
+        assert states.dtype == STATE_DTYPE and states.flags.c_contiguous
+        sums = np.empty(len(states), np.uint64)
+        hist = np.empty((len(states), 256), np.uint32)
+        _check(lib().ranmar_ctx_consume(self._h, _ptr(states), len(states), per_stream,
+                                        _ptr(sums), _ptr(hist)))
+        return sums, hist

@@ -1,0 +1,771 @@
+// Host runtime behind the C ABI (include/ranmar_b200.h): argument checking
+// with the reference's error semantics, 256-bit jump-count arithmetic, the
+// stream-range planner for make_streams, kernel orchestration on the caller's
+// stream, and the host-buffer (ctx) pipeline. No compute of the hot path runs
+// here: generation and jumps are the sm_100a kernels in gen_kernels.cu and
+// jump_kernels.cu. The only host arithmetic is the cold seed expansion
+// (init.hpp:18-51, ~15 us), closed-form residues mod m, and text persistence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "ranmar_b200.h"
+
+namespace rb {
+struct PowJob {
+    uint64_t e[4];
+    int extra;
+    uint32_t* out;
+};
+struct PowJobs {
+    PowJob job[2];
+};
+template <class T>
+cudaError_t launch_generate(ranmar_state*, uint64_t, uint64_t, T*, uint32_t*, cudaStream_t);
+cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_t*, uint32_t*,
+                           cudaStream_t);
+cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
+                            cudaStream_t);
+cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
+cudaError_t launch_t_table(uint32_t*, uint32_t*, const uint32_t*, cudaStream_t);
+cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
+                         cudaStream_t);
+cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
+cudaError_t launch_bulk(const ranmar_state*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
+                        uint64_t, uint32_t, uint32_t, const ranmar_state&, int, cudaStream_t);
+std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+}  // namespace rb
+
+namespace {
+
+constexpr uint32_t kMask = 0x00FFFFFFu;
+constexpr uint32_t kMod = 16777213u;
+constexpr uint32_t kDelta = 7654321u;
+constexpr uint32_t kStart = 362436u;
+constexpr uint32_t kMaxSeed = 900000000u;
+constexpr int kRows = 128;      // must match jump_kernels.cu
+constexpr int kPolyN = 97;
+constexpr int kJPad = 104;
+
+static_assert(sizeof(ranmar_state) == 400, "ranmar_state must be the 400-B RanmarState");
+static_assert(sizeof(ranmar_gauss_state) == 416, "ranmar_gauss_state layout");
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(RANMAR_ECUDA, std::string("ranmar: ") + what + ": " + cudaGetErrorString(e));
+}
+
+#define RB_CUDA(call, what)                          \
+    do {                                             \
+        cudaError_t e_ = (call);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+// ---- 256-bit jump counts ------------------------------------------------
+struct U256 {
+    uint64_t w[4];
+};
+
+U256 from_abi(const ranmar_jump_count* j) {
+    U256 r;
+    std::memcpy(r.w, j->limb, sizeof r.w);
+    return r;
+}
+bool is_zero(const U256& a) { return (a.w[0] | a.w[1] | a.w[2] | a.w[3]) == 0; }
+uint32_t mod_u32(const U256& a, uint32_t m) {
+    unsigned __int128 r = 0;
+    for (int k = 3; k >= 0; --k) r = ((r << 64) | a.w[k]) % m;
+    return static_cast<uint32_t>(r);
+}
+// a * k; returns false on overflow past 256 bits.
+bool mul_u64(const U256& a, uint64_t k, U256* out) {
+    unsigned __int128 carry = 0;
+    U256 r;
+    for (int i = 0; i < 4; ++i) {
+        const unsigned __int128 p = static_cast<unsigned __int128>(a.w[i]) * k + carry;
+        r.w[i] = static_cast<uint64_t>(p);
+        carry = p >> 64;
+    }
+    *out = r;
+    return carry == 0;
+}
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
+    return static_cast<uint64_t>(static_cast<unsigned __int128>(a) * b % m);
+}
+// (J mod m) * d mod m: the per-jump decrement of the arithmetic part (jump.hpp:82-84).
+uint32_t arith_dec(uint32_t jm) { return static_cast<uint32_t>(mulmod(jm, kDelta, kMod)); }
+
+// ---- per-device status word and SM count ---------------------------------
+std::mutex g_dev_mu;
+uint32_t* g_status[64] = {};
+int g_sms[64] = {};
+
+int device_status_ptr(uint32_t** out, int* sms) {
+    int dev = 0;
+    RB_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(RANMAR_ECUDA, "ranmar: device index out of range");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_status[dev]) {
+        uint32_t* p = nullptr;
+        RB_CUDA(cudaMalloc(&p, 256), "cudaMalloc(status)");
+        RB_CUDA(cudaMemset(p, 0, 256), "cudaMemset(status)");
+        RB_CUDA(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev),
+                "cudaDeviceGetAttribute");
+        g_status[dev] = p;
+    }
+    *out = g_status[dev];
+    if (sms) *sms = g_sms[dev];
+    return RANMAR_OK;
+}
+
+// ---- make_streams workspace plan -----------------------------------------
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Plan {
+    uint64_t H;     // anchors (ceil(n / 128))
+    int anchor_levels;
+    int B;          // Q_b = P_{2^b J}, b < B
+    size_t off_q, off_pfirst, off_t, off_tt, off_anchor, off_base, total;
+};
+
+Plan plan_for(uint64_t n) {
+    Plan p{};
+    p.H = (n + kRows - 1) / kRows;
+    p.anchor_levels = 0;
+    while ((uint64_t(1) << p.anchor_levels) < p.H) ++p.anchor_levels;
+    p.B = 7 + p.anchor_levels;  // T table uses Q_0..Q_6; anchor level b uses Q_{b+7}
+    size_t o = 0;
+    p.off_q = o;
+    o = align256(o + size_t(p.B) * kPolyN * 4);
+    p.off_pfirst = o;
+    o = align256(o + kPolyN * 4);
+    p.off_t = o;
+    o = align256(o + size_t(kRows) * kPolyN * 4);
+    p.off_tt = o;
+    o = align256(o + size_t(kJPad) * kRows * 4);
+    p.off_anchor = o;
+    o = align256(o + size_t(p.H) * sizeof(ranmar_state));
+    p.off_base = o;
+    o = align256(o + sizeof(ranmar_state));
+    p.total = o;
+    return p;
+}
+
+void seed_expand(uint32_t seed, ranmar_state* out) {
+    // init.hpp:22-49 (signed split with C++ truncation; Remainder form of the mixer).
+    const int ij = (static_cast<int>(seed) - 1) / 30082;
+    const int kl = (static_cast<int>(seed) - 1) - 30082 * ij;
+    int ii = (ij / 177) % 177 + 2, jj = ij % 177 + 2, kk = (kl / 169) % 178 + 1, ll = kl % 169;
+    std::memset(out, 0, sizeof *out);
+    for (int lane = 0; lane < 97; ++lane) {
+        uint32_t acc = 0, t = 1u << 31;
+        for (int bit = 0; bit < 24; ++bit) {
+            const int mm = ((ii * jj) % 179) * kk % 179;
+            ii = jj;
+            jj = kk;
+            kk = mm;
+            ll = (53 * ll + 1) % 169;
+            if ((ll * mm) % 64 >= 32) acc += t;
+            t >>= 1;
+        }
+        out->lane[lane] = acc >> 8;
+    }
+    out->i = 96;
+    out->j = 32;
+    out->v = kStart;
+}
+
+bool host_state_ok(const ranmar_state& s) {
+    return s.i >= 0 && s.i < 97 && s.j >= 0 && s.j < 97 && (s.i - s.j + 97) % 97 == 64 &&
+           s.v < kMod;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int ranmar_abi_version(void) { return RANMAR_ABI_VERSION; }
+uint64_t ranmar_kernel_launches(void) { return rb::g_launches.load(); }
+const char* ranmar_last_error(void) { return g_error.c_str(); }
+
+int ranmar_init(uint32_t seed, ranmar_state* out) {
+    if (!out) return fail(RANMAR_EINVAL, "ranmar: null output");
+    if (seed > kMaxSeed) return fail(RANMAR_EINVAL, "ranmar: seed must be in [0, 900000000]");
+    seed_expand(seed, out);
+    return RANMAR_OK;
+}
+
+int ranmar_init_unchecked(uint32_t seed, ranmar_state* out) {
+    if (!out) return fail(RANMAR_EINVAL, "ranmar: null output");
+    seed_expand(seed, out);
+    return RANMAR_OK;
+}
+
+int ranmar_value_of(uint32_t u24, double* out) {
+    if (u24 > kMask) return fail(RANMAR_EINVAL, "ranmar: value_of argument exceeds 24 bits");
+    *out = static_cast<double>(u24) * 0x1p-24;
+    return RANMAR_OK;
+}
+
+int ranmar_parse_jump_count(const char* text, ranmar_jump_count* out) {
+    // jumpcount.hpp:16-47: decimal, "2^k", "2^k-1", "2^k+1" (k <= 10^6 there).
+    std::memset(out, 0, sizeof *out);
+    const std::string bad = std::string("ranmar: bad jump count \"") + (text ? text : "") +
+                            "\" (want decimal, 2^k, 2^k-1, or 2^k+1)";
+    if (!text || !*text) return fail(RANMAR_EINVAL, bad);
+    if (text[0] == '2' && text[1] == '^') {
+        const char* p = text + 2;
+        unsigned long k = 0;
+        int nd = 0;
+        while (*p >= '0' && *p <= '9') {
+            k = k * 10 + static_cast<unsigned long>(*p - '0');
+            if (k > 1000000) return fail(RANMAR_EINVAL, "ranmar: jump exponent too large");
+            ++p;
+            ++nd;
+        }
+        if (nd == 0) return fail(RANMAR_EINVAL, bad);
+        int delta = 0;
+        if (std::strcmp(p, "-1") == 0) delta = -1;
+        else if (std::strcmp(p, "+1") == 0) delta = 1;
+        else if (*p) return fail(RANMAR_EINVAL, bad);
+        if (k > 256 || (k == 256 && delta >= 0))
+            return fail(RANMAR_ERANGE, "ranmar: jump count exceeds 2^256 - 1");
+        if (k < 256) out->limb[k / 64] = uint64_t(1) << (k % 64);
+        if (delta == 1) {
+            for (int w = 0; w < 4; ++w)
+                if (++out->limb[w] != 0) break;
+        } else if (delta == -1) {
+            for (int w = 0; w < 4; ++w)
+                if (out->limb[w]-- != 0) break;
+        }
+        return RANMAR_OK;
+    }
+    for (const char* p = text; *p; ++p)
+        if (*p < '0' || *p > '9') return fail(RANMAR_EINVAL, bad);
+    U256 acc{};
+    for (const char* p = text; *p; ++p) {
+        U256 t;
+        if (!mul_u64(acc, 10, &t)) return fail(RANMAR_ERANGE, "ranmar: jump count exceeds 2^256 - 1");
+        unsigned __int128 carry = static_cast<unsigned>(*p - '0');
+        for (int w = 0; w < 4; ++w) {
+            const unsigned __int128 s = static_cast<unsigned __int128>(t.w[w]) + carry;
+            t.w[w] = static_cast<uint64_t>(s);
+            carry = s >> 64;
+        }
+        if (carry) return fail(RANMAR_ERANGE, "ranmar: jump count exceeds 2^256 - 1");
+        acc = t;
+    }
+    std::memcpy(out->limb, acc.w, sizeof acc.w);
+    return RANMAR_OK;
+}
+
+int ranmar_jump_arith(uint32_t v, const ranmar_jump_count* j, uint32_t* out) {
+    if (!j || !out) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    const uint32_t dec = arith_dec(mod_u32(from_abi(j), kMod));
+    *out = static_cast<uint32_t>((uint64_t(v) + (kMod - dec)) % kMod);
+    return RANMAR_OK;
+}
+
+long ranmar_to_text(const ranmar_state* s, char* buf, long cap) {
+    // serialize.hpp:21-40
+    std::string out = "ranmar24 v1\ni " + std::to_string(s->i + 1) + " j " +
+                      std::to_string(s->j + 1) + "\nv " + std::to_string(s->v) + "\n";
+    for (int k = 0; k < 97; ++k)
+        out += "u " + std::to_string(k + 1) + " " + std::to_string(s->lane[k]) + "\n";
+    if (static_cast<long>(out.size()) + 1 > cap) return -1;
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+    return static_cast<long>(out.size());
+}
+
+int ranmar_from_text(const char* text, ranmar_state* out) {
+    // serialize.hpp:81-136: strict, line-based; EINVAL with the line number.
+    int line = 1;
+    const char* t = text ? text : "";
+    auto perr = [&](const std::string& what) {
+        return fail(RANMAR_EINVAL,
+                    "ranmar: state parse error at line " + std::to_string(line) + ": " + what);
+    };
+    auto next_line = [&](std::string& l) -> bool {
+        if (!*t) return false;
+        const char* nl = std::strchr(t, '\n');
+        size_t n = nl ? size_t(nl - t) : std::strlen(t);
+        l.assign(t, n);
+        t = nl ? nl + 1 : t + n;
+        if (!l.empty() && l.back() == '\r') l.pop_back();
+        return true;
+    };
+    auto take_uint = [&](const std::string& l, size_t& pos, uint64_t& v) -> bool {
+        v = 0;
+        size_t n = 0;
+        while (pos < l.size() && l[pos] >= '0' && l[pos] <= '9') {
+            v = v * 10 + uint64_t(l[pos] - '0');
+            if (v > 0xFFFFFFFFull) return false;
+            ++pos;
+            ++n;
+        }
+        return n > 0;
+    };
+    auto take_lit = [&](const std::string& l, size_t& pos, const char* lit) -> bool {
+        const size_t n = std::strlen(lit);
+        if (l.compare(pos, n, lit) != 0) return false;
+        pos += n;
+        return true;
+    };
+    std::string l;
+    if (!next_line(l)) return perr("unexpected end of input");
+    if (l != "ranmar24 v1") return perr("bad magic (want \"ranmar24 v1\")");
+    ranmar_state s{};
+    ++line;
+    if (!next_line(l)) return perr("unexpected end of input");
+    size_t pos = 0;
+    uint64_t i = 0, j = 0, v = 0;
+    if (!take_lit(l, pos, "i ")) return perr("expected \"i \"");
+    if (!take_uint(l, pos, i)) return perr("expected a decimal number");
+    if (!take_lit(l, pos, " j ")) return perr("expected \" j \"");
+    if (!take_uint(l, pos, j)) return perr("expected a decimal number");
+    if (pos != l.size()) return perr("trailing characters");
+    if (i < 1 || i > 97 || j < 1 || j > 97) return perr("cursor out of range");
+    if ((i + 97 - j) % 97 != 64) return perr("cursor separation must be 64");
+    s.i = int32_t(i) - 1;
+    s.j = int32_t(j) - 1;
+    ++line;
+    if (!next_line(l)) return perr("unexpected end of input");
+    pos = 0;
+    if (!take_lit(l, pos, "v ")) return perr("expected \"v \"");
+    if (!take_uint(l, pos, v)) return perr("expected a decimal number");
+    if (pos != l.size()) return perr("trailing characters");
+    if (v >= kMod) return perr("v must be < 16777213");
+    s.v = uint32_t(v);
+    for (int k = 0; k < 97; ++k) {
+        ++line;
+        if (!next_line(l)) return perr("unexpected end of input");
+        pos = 0;
+        uint64_t idx = 0, lane = 0;
+        if (!take_lit(l, pos, "u ")) return perr("expected \"u \"");
+        if (!take_uint(l, pos, idx)) return perr("expected a decimal number");
+        if (!take_lit(l, pos, " ")) return perr("expected \" \"");
+        if (!take_uint(l, pos, lane)) return perr("expected a decimal number");
+        if (pos != l.size()) return perr("trailing characters");
+        if (idx != uint64_t(k) + 1) return perr("lane index out of order");
+        if (lane > kMask) return perr("lane value exceeds 24 bits");
+        s.lane[k] = uint32_t(lane);
+    }
+    for (; *t; ++t)
+        if (*t != '\n' && *t != '\r' && *t != ' ' && *t != '\t') {
+            ++line;
+            return perr("trailing content after state");
+        }
+    *out = s;
+    return RANMAR_OK;
+}
+
+// ---------------------------------------------------------------- device
+
+size_t ranmar_make_streams_workspace(uint64_t n) { return plan_for(n ? n : 1).total; }
+
+int ranmar_pow_t_mod_dev(const ranmar_jump_count* j, uint32_t* d_coeff, void* stream) {
+    if (!j || !d_coeff) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    rb::PowJobs jobs{};
+    std::memcpy(jobs.job[0].e, j->limb, sizeof jobs.job[0].e);
+    jobs.job[0].extra = 0;
+    jobs.job[0].out = d_coeff;
+    RB_CUDA(rb::launch_pow(jobs, 1, static_cast<cudaStream_t>(stream)), "pow_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
+                    const ranmar_jump_count* j, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!j) return fail(RANMAR_EINVAL, "ranmar: null jump count");
+    if (n == 0) return RANMAR_OK;
+    if (!d_in || !d_out || !d_ws) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    if (ws_bytes < kPolyN * 4) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t* P = static_cast<uint32_t*>(d_ws);
+    int rc = ranmar_pow_t_mod_dev(j, P, stream);
+    if (rc) return rc;
+    const uint32_t dec = arith_dec(mod_u32(from_abi(j), kMod));
+    RB_CUDA(rb::launch_apply(d_in, d_out, n, P, dec, s), "apply_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j, uint64_t first,
+                            uint64_t n, ranmar_state* d_out, void* d_ws, size_t ws_bytes,
+                            void* stream) {
+    if (!base || !j) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    if (n == 0) return fail(RANMAR_EINVAL, "ranmar: need at least one stream");  // jump.hpp:111
+    const U256 J = from_abi(j);
+    if (is_zero(J)) return fail(RANMAR_EINVAL, "ranmar: block length must be >= 1");  // :112
+    if (!host_state_ok(*base))
+        return fail(RANMAR_ESTATE, "ranmar: base state violates cursor/residue invariants");
+    if (first >= (uint64_t(1) << 62) || n >= (uint64_t(1) << 62) || first + n >= (uint64_t(1) << 62))
+        return fail(RANMAR_ERANGE, "ranmar: stream range too large");
+    const Plan p = plan_for(n);
+    if (!d_out || !d_ws) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (ws_bytes < p.total) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
+    U256 fj;
+    if (!mul_u64(J, first, &fj)) return fail(RANMAR_ERANGE, "ranmar: first * J exceeds 2^256");
+    {   // every stream start (first + n - 1) * J must be representable too
+        U256 lastj;
+        if (!mul_u64(J, first + n - 1, &lastj))
+            return fail(RANMAR_ERANGE, "ranmar: (first + n - 1) * J exceeds 2^256");
+    }
+    int sms = 148;
+    uint32_t* status = nullptr;
+    if (int rc = device_status_ptr(&status, &sms)) return rc;
+    (void)status;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* ws = static_cast<char*>(d_ws);
+    uint32_t* Q = reinterpret_cast<uint32_t*>(ws + p.off_q);
+    uint32_t* Pf = reinterpret_cast<uint32_t*>(ws + p.off_pfirst);
+    uint32_t* T = reinterpret_cast<uint32_t*>(ws + p.off_t);
+    uint32_t* Tt = reinterpret_cast<uint32_t*>(ws + p.off_tt);
+    ranmar_state* A = reinterpret_cast<ranmar_state*>(ws + p.off_anchor);
+    ranmar_state* dbase = reinterpret_cast<ranmar_state*>(ws + p.off_base);
+
+    // K3a: Q_b = P_{2^b J} (b < B) and, if first > 0, P_{first J}.
+    rb::PowJobs jobs{};
+    std::memcpy(jobs.job[0].e, J.w, sizeof J.w);
+    jobs.job[0].extra = p.B - 1;
+    jobs.job[0].out = Q;
+    int njobs = 1;
+    if (first > 0) {
+        std::memcpy(jobs.job[1].e, fj.w, sizeof fj.w);
+        jobs.job[1].extra = 0;
+        jobs.job[1].out = Pf;
+        njobs = 2;
+    }
+    RB_CUDA(rb::launch_pow(jobs, njobs, s), "pow_kernel launch");
+    // Offset table T_r = P_{rJ}, r < 128, by doubling.
+    RB_CUDA(rb::launch_t_table(T, Tt, Q, s), "t_table launch");
+    // Anchors A_h = s_{(first + 128 h) J}: A_0, then doubling with Q_{b+7}.
+    const uint32_t jm = mod_u32(J, kMod);
+    if (first == 0) {
+        RB_CUDA(rb::launch_put_state(*base, A, s), "put_state launch");
+    } else {
+        RB_CUDA(rb::launch_put_state(*base, dbase, s), "put_state launch");
+        const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(first % kMod, jm, kMod)));
+        RB_CUDA(rb::launch_apply(dbase, A, 1, Pf, dec, s), "apply_kernel launch");
+    }
+    for (int b = 0; b < p.anchor_levels; ++b) {
+        const uint64_t half = uint64_t(1) << b;
+        const uint64_t count = std::min<uint64_t>(half, p.H - half);
+        // jump by 2^b * 128 * J: (2^(b+7) mod m) * (J mod m) mod m
+        uint64_t pw = 1;
+        for (int x = 0; x < b + 7; ++x) pw = pw * 2 % kMod;
+        const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(pw, jm, kMod)));
+        RB_CUDA(rb::launch_apply(A, A + half, count, Q + size_t(b + 7) * kPolyN, dec, s),
+                "apply_kernel launch");
+    }
+    // Bulk: every stream start.
+    RB_CUDA(rb::launch_bulk(A, p.H, Tt, d_out, first, n, base->v, jm, *base, sms, s),
+            "bulk_kernel launch");
+    return RANMAR_OK;
+}
+
+#define RB_STATUS_PTR(var)                               \
+    uint32_t* var = nullptr;                             \
+    if (int rc_ = device_status_ptr(&var, nullptr)) return rc_
+
+int ranmar_generate_u32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            uint32_t* d_out, void* stream) {
+    if (n_streams && (!d_states || (per_stream && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_generate<uint32_t>(d_states, n_streams, per_stream, d_out, status,
+                                          static_cast<cudaStream_t>(stream)),
+            "gen_store_kernel<u32> launch");
+    return RANMAR_OK;
+}
+
+int ranmar_generate_f32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            float* d_out, void* stream) {
+    if (n_streams && (!d_states || (per_stream && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_generate<float>(d_states, n_streams, per_stream, d_out, status,
+                                       static_cast<cudaStream_t>(stream)),
+            "gen_store_kernel<f32> launch");
+    return RANMAR_OK;
+}
+
+int ranmar_generate_f64_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                            double* d_out, void* stream) {
+    if (n_streams && (!d_states || (per_stream && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_generate<double>(d_states, n_streams, per_stream, d_out, status,
+                                        static_cast<cudaStream_t>(stream)),
+            "gen_store_kernel<f64> launch");
+    return RANMAR_OK;
+}
+
+int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                       uint64_t* d_sums, uint32_t* d_hist, void* stream) {
+    if (n_streams && (!d_states || !d_sums || !d_hist))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_consume(d_states, n_streams, per_stream, d_sums, d_hist, status,
+                               static_cast<cudaStream_t>(stream)),
+            "consume_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
+                            uint64_t steps, double* d_out, void* stream) {
+    if (n_atoms && (!d_g || (per_step && steps && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
+                                static_cast<cudaStream_t>(stream)),
+            "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_device_status(uint32_t* flags, int clear) {
+    RB_STATUS_PTR(status);
+    RB_CUDA(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    uint32_t h = 0;
+    RB_CUDA(cudaMemcpy(&h, status, 4, cudaMemcpyDeviceToHost), "cudaMemcpy(status)");
+    if (clear) RB_CUDA(cudaMemset(status, 0, 4), "cudaMemset(status)");
+    if (flags) *flags = h;
+    return RANMAR_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- host-buffer context
+struct ranmar_ctx {
+    int device = 0;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    void* dbuf[2] = {nullptr, nullptr};  // per-slot output chunk
+    size_t dbuf_bytes = 0;
+    ranmar_state* dstates = nullptr;
+    size_t dstates_n = 0;
+    void* dws = nullptr;
+    size_t dws_bytes = 0;
+    uint64_t h2d = 0, d2h = 0;
+};
+
+namespace {
+
+int ctx_reserve(void** p, size_t* have, size_t need) {
+    if (*have >= need) return RANMAR_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    RB_CUDA(cudaMalloc(p, need), "cudaMalloc(ctx)");
+    *have = need;
+    return RANMAR_OK;
+}
+
+int ctx_states(ranmar_ctx* c, uint64_t n) {
+    size_t have = c->dstates_n * sizeof(ranmar_state);
+    void* p = c->dstates;
+    int rc = ctx_reserve(&p, &have, n * sizeof(ranmar_state));
+    c->dstates = static_cast<ranmar_state*>(p);
+    c->dstates_n = have / sizeof(ranmar_state);
+    return rc;
+}
+
+constexpr size_t kChunkBytes = size_t(512) << 20;  // output bytes per pipelined chunk
+
+template <class T>
+int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream, T* h_out,
+                 int (*gen)(ranmar_state*, uint64_t, uint64_t, T*, void*)) {
+    if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
+    c->h2d = c->d2h = 0;
+    if (n == 0) return RANMAR_OK;
+    if (!h_states || (per_stream && !h_out)) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    for (uint64_t k = 0; k < n; ++k)
+        if (!host_state_ok(h_states[k]))
+            return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
+                                           " violates cursor/residue invariants");
+    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t stream_bytes = per_stream * sizeof(T);
+    uint64_t chunk = stream_bytes ? std::max<uint64_t>(1, kChunkBytes / stream_bytes) : n;
+    chunk = std::min<uint64_t>(chunk, n);
+    if (int rc = ctx_states(c, n)) return rc;
+    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes, chunk * stream_bytes)) return rc;
+    if (c->dbuf[1] == nullptr || c->dbuf_bytes < chunk * stream_bytes) {
+        if (c->dbuf[1]) cudaFree(c->dbuf[1]);
+        c->dbuf[1] = nullptr;
+        RB_CUDA(cudaMalloc(&c->dbuf[1], c->dbuf_bytes), "cudaMalloc(ctx)");
+    }
+    RB_CUDA(cudaMemcpyAsync(c->dstates, h_states, n * sizeof(ranmar_state),
+                            cudaMemcpyHostToDevice, c->st[0]),
+            "H2D states");
+    RB_CUDA(cudaEventRecord(c->ev[0], c->st[0]), "cudaEventRecord");
+    RB_CUDA(cudaStreamWaitEvent(c->st[1], c->ev[0], 0), "cudaStreamWaitEvent");
+    c->h2d += n * sizeof(ranmar_state);
+    // Slot s alternates streams: generation of chunk q+1 overlaps the copy-out of chunk q.
+    int q = 0;
+    for (uint64_t k0 = 0; k0 < n; k0 += chunk, ++q) {
+        const uint64_t cnt = std::min<uint64_t>(chunk, n - k0);
+        const int slot = q & 1;
+        cudaStream_t s = c->st[slot];
+        T* dout = static_cast<T*>(c->dbuf[slot]);
+        if (int rc = gen(c->dstates + k0, cnt, per_stream, dout, s)) return rc;
+        RB_CUDA(cudaMemcpyAsync(h_out + k0 * per_stream, dout, cnt * stream_bytes,
+                                cudaMemcpyDeviceToHost, s),
+                "D2H output");
+        c->d2h += cnt * stream_bytes;
+    }
+    RB_CUDA(cudaStreamSynchronize(c->st[1]), "sync");
+    RB_CUDA(cudaMemcpyAsync(h_states, c->dstates, n * sizeof(ranmar_state),
+                            cudaMemcpyDeviceToHost, c->st[0]),
+            "D2H states");
+    c->d2h += n * sizeof(ranmar_state);
+    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
+    uint32_t flags = 0;
+    if (int rc = ranmar_device_status(&flags, 1)) return rc;
+    if (flags) return fail(RANMAR_ESTATE, "ranmar: a device state violated the invariants");
+    return RANMAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ranmar_ctx_create(int device, ranmar_ctx** out) {
+    if (!out) return fail(RANMAR_EINVAL, "ranmar: null output");
+    int count = 0;
+    RB_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) return fail(RANMAR_ECUDA, "ranmar: no such CUDA device");
+    RB_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    ranmar_ctx* c = new (std::nothrow) ranmar_ctx();
+    if (!c) return fail(RANMAR_ENOMEM, "ranmar: out of host memory");
+    c->device = device;
+    for (int i = 0; i < 2; ++i) {
+        RB_CUDA(cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking), "cudaStreamCreate");
+        RB_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    *out = c;
+    return RANMAR_OK;
+}
+
+void ranmar_ctx_destroy(ranmar_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < 2; ++i) {
+        if (c->st[i]) cudaStreamDestroy(c->st[i]);
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+        if (c->dbuf[i]) cudaFree(c->dbuf[i]);
+    }
+    if (c->dstates) cudaFree(c->dstates);
+    if (c->dws) cudaFree(c->dws);
+    delete c;
+}
+
+int ranmar_ctx_last_traffic(ranmar_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+    if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
+    if (h2d) *h2d = c->h2d;
+    if (d2h) *d2h = c->d2h;
+    return RANMAR_OK;
+}
+
+int ranmar_ctx_make_streams(ranmar_ctx* c, uint32_t seed, const ranmar_jump_count* j,
+                            uint64_t first, uint64_t n, ranmar_state* h_out) {
+    if (!c || !h_out) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    c->h2d = c->d2h = 0;
+    ranmar_state base;
+    if (int rc = ranmar_init(seed, &base)) return rc;  // init.hpp:19-20 range check
+    if (n == 0) return fail(RANMAR_EINVAL, "ranmar: need at least one stream");
+    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    if (int rc = ctx_states(c, n)) return rc;
+    if (int rc = ctx_reserve(&c->dws, &c->dws_bytes, ranmar_make_streams_workspace(n))) return rc;
+    if (int rc = ranmar_make_streams_dev(&base, j, first, n, c->dstates, c->dws, c->dws_bytes,
+                                         c->st[0]))
+        return rc;
+    RB_CUDA(cudaMemcpyAsync(h_out, c->dstates, n * sizeof(ranmar_state), cudaMemcpyDeviceToHost,
+                            c->st[0]),
+            "D2H states");
+    c->d2h += n * sizeof(ranmar_state);
+    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
+    return RANMAR_OK;
+}
+
+int ranmar_ctx_jump(ranmar_ctx* c, const ranmar_state* h_in, ranmar_state* h_out, uint64_t n,
+                    const ranmar_jump_count* j) {
+    if (!c || !j) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    c->h2d = c->d2h = 0;
+    if (n == 0) return RANMAR_OK;
+    if (!h_in || !h_out) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    for (uint64_t k = 0; k < n; ++k)
+        if (!host_state_ok(h_in[k]))
+            return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
+                                           " violates cursor/residue invariants");
+    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    if (int rc = ctx_states(c, n)) return rc;
+    if (int rc = ctx_reserve(&c->dws, &c->dws_bytes, 4096)) return rc;
+    RB_CUDA(cudaMemcpyAsync(c->dstates, h_in, n * sizeof(ranmar_state), cudaMemcpyHostToDevice,
+                            c->st[0]),
+            "H2D states");
+    c->h2d += n * sizeof(ranmar_state);
+    if (int rc = ranmar_jump_dev(c->dstates, c->dstates, n, j, c->dws, c->dws_bytes, c->st[0]))
+        return rc;
+    RB_CUDA(cudaMemcpyAsync(h_out, c->dstates, n * sizeof(ranmar_state), cudaMemcpyDeviceToHost,
+                            c->st[0]),
+            "D2H states");
+    c->d2h += n * sizeof(ranmar_state);
+    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
+    return RANMAR_OK;
+}
+
+int ranmar_ctx_generate_u32(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
+                            uint32_t* h_out) {
+    return ctx_generate<uint32_t>(c, h_states, n, per_stream, h_out, ranmar_generate_u32_dev);
+}
+
+int ranmar_ctx_generate_f32(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
+                            float* h_out) {
+    return ctx_generate<float>(c, h_states, n, per_stream, h_out, ranmar_generate_f32_dev);
+}
+
+int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
+                       uint64_t* h_sums, uint32_t* h_hist) {
+    if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
+    c->h2d = c->d2h = 0;
+    if (n == 0) return RANMAR_OK;
+    if (!h_states || !h_sums || !h_hist) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    for (uint64_t k = 0; k < n; ++k)
+        if (!host_state_ok(h_states[k]))
+            return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
+                                           " violates cursor/residue invariants");
+    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    if (int rc = ctx_states(c, n)) return rc;
+    const size_t need = n * (8 + 256 * 4);
+    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes, need)) return rc;
+    uint64_t* dsums = static_cast<uint64_t*>(c->dbuf[0]);
+    uint32_t* dhist = reinterpret_cast<uint32_t*>(dsums + n);
+    cudaStream_t s = c->st[0];
+    RB_CUDA(cudaMemcpyAsync(c->dstates, h_states, n * sizeof(ranmar_state), cudaMemcpyHostToDevice,
+                            s),
+            "H2D states");
+    c->h2d += n * sizeof(ranmar_state);
+    if (int rc = ranmar_consume_dev(c->dstates, n, per_stream, dsums, dhist, s)) return rc;
+    RB_CUDA(cudaMemcpyAsync(h_sums, dsums, n * 8, cudaMemcpyDeviceToHost, s), "D2H sums");
+    RB_CUDA(cudaMemcpyAsync(h_hist, dhist, n * 256 * 4, cudaMemcpyDeviceToHost, s), "D2H hist");
+    RB_CUDA(cudaMemcpyAsync(h_states, c->dstates, n * sizeof(ranmar_state), cudaMemcpyDeviceToHost,
+                            s),
+            "D2H states");
+    c->d2h += n * (8 + 256 * 4 + sizeof(ranmar_state));
+    RB_CUDA(cudaStreamSynchronize(s), "sync");
+    return RANMAR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the oracle
+(oracle/ranmar_oracle.c, itself pinned to the reference) and the reference's
+golden vectors. Integer/byte results must be bit-exact; gaussian() is within
+1 ulp (the only non-exact step is log(): CUDA's vs glibc's)."""
+import random
+
+import numpy as np
+import pytest
+
+import paper_2512_00093_b200 as rb
+from oracle.bind import STATE_DTYPE
+from ranmar_testutil import state_from_json
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU-only module
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(autouse=True)
+def _clean_status():
+    rb.device_status(clear=True)
+    yield
+    torch.cuda.synchronize()
+    assert rb.device_status(clear=True) == 0, "a kernel flagged an invalid state"
+
+
+def random_states(n, seed, oracle):
+    """Valid states with random lanes and random cursor phase (test_util.hpp:20-27)."""
+    rng = np.random.default_rng(seed)
+    s = np.zeros(n, STATE_DTYPE)
+    s["lane"] = rng.integers(0, 1 << 24, (n, 97), dtype=np.uint32)
+    s["i"] = rng.integers(0, 97, n)
+    s["j"] = (s["i"] + 97 - 64) % 97
+    s["v"] = rng.integers(0, 16777213, n, dtype=np.uint32)
+    return s
+
+
+# ---------------------------------------------------------------- K3 jump
+
+def test_pow_t_mod_golden(refvec):
+    for case in refvec["pow_t_mod"]:
+        got = rb.pow_t_mod_dev(int(case["j"])).cpu().numpy().view(np.uint32)
+        assert got.tolist() == case["coeff"], case["j"]
+
+
+def test_jump_golden(refvec):
+    for case in refvec["jump_state"]:
+        got = rb.jump_state(state_from_json(case["in"]), int(case["j"]))
+        assert got.tobytes() == state_from_json(case["out"]).tobytes(), case["j"]
+
+
+def test_jump_matches_stepping(oracle):
+    # acceptance.cpp:94-108: J <= 10^4 against literal stepping, random states.
+    base = random_states(40, 1, oracle)
+    d = rb.states_to_device(base)
+    for j in (0, 1, 2, 33, 64, 97, 98, 1000, 10_000):
+        got = rb.states_to_host(rb.jump_dev(d, j))
+        for k in range(len(base)):
+            a = base[k:k + 1].copy()
+            oracle.step_n(a, j)
+            b = got[k:k + 1].copy()
+            assert (oracle.step_n(a, 100) == oracle.step_n(b, 100)).all(), (j, k)
+            assert got[k:k + 1].tobytes() == oracle.jump_state(base[k:k + 1], j).tobytes()
+
+
+def test_jump_large_and_additive(oracle):
+    base = random_states(300, 2, oracle)
+    d = rb.states_to_device(base)
+    rng = random.Random(3)
+    for j in [2**40, 2**64 - 1, 2**120, 2**120 - 1, rng.getrandbits(141)]:
+        got = rb.states_to_host(rb.jump_dev(d, j))
+        for k in range(0, len(base), 37):
+            assert got[k:k + 1].tobytes() == oracle.jump_state(base[k:k + 1], j).tobytes()
+    # additivity (acceptance.cpp:110-118): (2^64-1) twice == 2^65-2 once
+    big = 2**64 - 1
+    twice = rb.jump_dev(rb.jump_dev(d, big), big)
+    once = rb.jump_dev(d, 2**65 - 2)
+    assert torch.equal(twice, once)
+    # in place
+    d2 = d.clone()
+    rb.jump_dev(d2, 12345, out=d2)
+    assert torch.equal(d2, rb.jump_dev(d, 12345))
+
+
+def test_make_streams_golden(refvec):
+    for case in refvec["make_streams"]:
+        got = rb.states_to_host(rb.make_streams(case["seed"], int(case["j"]), len(case["states"])))
+        for g, e in zip(got, case["states"]):
+            assert g.tobytes() == state_from_json(e).tobytes()
+
+
+@pytest.mark.parametrize("n,first", [(1, 0), (2, 0), (127, 0), (128, 0), (129, 0), (300, 0),
+                                     (1000, 0), (200, 5), (257, 1000), (1, 77)])
+def test_make_streams_shapes(oracle, n, first):
+    base = oracle.init(12345)
+    got = rb.states_to_host(rb.make_streams_dev(base, 2**40, n, first=first))
+    exp = oracle.make_streams(base, 2**40, n, first=first)
+    assert got.tobytes() == exp.tobytes()
+
+
+def test_make_streams_from_phased_base(oracle):
+    # a base with a non-fresh cursor phase: stream 0 is the base verbatim
+    base = oracle.init(4711)
+    oracle.step_n(base, 40)
+    got = rb.states_to_host(rb.make_streams_dev(base, 1000, 300))
+    assert got.tobytes() == oracle.make_streams(base, 1000, 300).tobytes()
+
+
+def test_make_streams_tiling(oracle):
+    # acceptance.cpp:195-206: stream blocks tile the base sequence
+    streams = rb.states_to_host(rb.make_streams(97531, 1000, 10))
+    base = oracle.step_n(oracle.init(97531), 10_000)
+    tiled = np.concatenate([oracle.step_n(streams[k:k + 1].copy(), 1000) for k in range(10)])
+    assert (tiled == base).all()
+
+
+def test_make_streams_errors():
+    with pytest.raises(ValueError):
+        rb.make_streams(1, 5, 0)  # jump.hpp:111
+    with pytest.raises(ValueError):
+        rb.make_streams(1, 0, 3)  # jump.hpp:112
+    with pytest.raises(ValueError):
+        rb.make_streams(900000001, 5, 3)  # init.hpp:19-20
+
+
+def test_config3_full(refvec):
+    # BASELINE config 3 at full size: 2^20 stream starts at J = 2^120.
+    c3 = refvec["c3_starts"]
+    base = rb.init_unchecked(c3["seed"])
+    n = 1 << 20
+    d = rb.make_streams_dev(base, int(c3["j"]), n)
+    host = rb.states_to_host(d)
+    for k, e in zip(c3["k"], c3["states"]):
+        assert host[k:k + 1].tobytes() == state_from_json(e).tobytes(), k
+    # size-independent property: s_{k+1} = jump(s_k, J) for every k
+    nxt = rb.jump_dev(d[:-1], int(c3["j"]))
+    assert torch.equal(nxt, d[1:])
+
+
+# ---------------------------------------------------------- K1 generation
+
+@pytest.mark.parametrize("fmt", ["u32", "f32", "f64"])
+@pytest.mark.parametrize("per_stream", [0, 1, 5, 31, 32, 33, 96, 97, 98, 128, 129, 1000, 4103])
+def test_generate_shapes(oracle, fmt, per_stream):
+    base = np.concatenate([oracle.init(12345), random_states(13, per_stream + 7, oracle)])
+    d = rb.states_to_device(base)
+    out = rb.generate(d, per_stream, fmt).cpu().numpy()
+    exp_states = base.copy()
+    exp_u = oracle.generate_u32(exp_states, per_stream)
+    if fmt == "u32":
+        assert (out.view(np.uint32) == exp_u).all()
+    elif fmt == "f32":
+        assert (out == (exp_u.astype(np.float64) * 2.0**-24).astype(np.float32)).all()
+    else:
+        assert (out == exp_u.astype(np.float64) * 2.0**-24).all()
+    # states advance exactly as step() leaves them (ring, cursors, v)
+    assert rb.states_to_host(d).tobytes() == exp_states.tobytes()
+
+
+def test_config1_integer_and_float(refvec, oracle):
+    # BASELINE config 1: one stream, seed 12345, 10^8 uniforms; integer path vs
+    # the reference summary, f32 path vs the float recurrence (float_ranmar.hpp).
+    c = refvec["c1_seed12345_1e8"]
+    d = rb.states_to_device(oracle.init(12345))
+    u = rb.generate(d, 10**8, "u32")
+    u64 = u.to(torch.int64) & 0xFFFFFFFF
+    assert int(u64.sum()) == c["sum"]
+    x = 0
+    for chunk in u64.split(1 << 24):
+        x ^= int(np.bitwise_xor.reduce(chunk.cpu().numpy()))
+    assert x == c["xor"] and int(u64[-1]) == c["last"]
+    assert rb.states_to_host(d).tobytes() == state_from_json(c["final_state"]).tobytes()
+    d2 = rb.states_to_device(oracle.init(12345))
+    f = rb.generate(d2, 10**8, "f32")
+    assert torch.equal((f.double() * 2.0**24).to(torch.int64), u64)
+    fl = oracle.float_outputs(12345, 10**6)
+    assert (f[:10**6].cpu().numpy().astype(np.float64) == fl).all()
+
+
+def test_config2_scaled(oracle):
+    # config 2 at 1/256 of the streams: make_streams(12345, 2^40, 256), 65536 fp32 each
+    states = rb.make_streams(12345, 2**40, 256)
+    out = rb.generate(states, 65536, "f32").cpu().numpy()
+    exp_states = oracle.make_streams(oracle.init(12345), 2**40, 256)
+    exp = oracle.generate_f32(exp_states, 65536)
+    assert (out == exp).all()
+    assert rb.states_to_host(states).tobytes() == exp_states.tobytes()
+
+
+def test_config2_full(refvec):
+    # config 2 at full size (2^32 fp32 = 16 GiB): per-stream sums of the stored
+    # values against the reference's (a checksum of checksums).
+    c = refvec["c2_full"]
+    n, per = c["n"], c["per_stream"]
+    states = rb.make_streams(c["seed"], int(c["j"]), n)
+    out = rb.generate(states, per, "f32")
+    sums = torch.empty(n, dtype=torch.int64, device="cuda")
+    for k0 in range(0, n, 4096):
+        blk = out[k0 * per:(k0 + 4096) * per].view(4096, per)
+        sums[k0:k0 + 4096] = (blk.double() * 2.0**24).to(torch.int64).sum(dim=1)
+    s = sums.cpu().numpy().astype(object)
+    assert int(sum(s)) == c["total_sum"]
+    assert [int(x) for x in s[:8]] == c["first_sums"]
+    assert sum((k + 1) * int(x) for k, x in enumerate(s)) & ((1 << 64) - 1) == c["weighted_digest"]
+    del out
+
+
+# --------------------------------------------------------------- K2 consume
+
+@pytest.mark.parametrize("per_stream", [0, 1, 31, 4096, 100_003])
+def test_consume_shapes(oracle, per_stream):
+    base = random_states(9, per_stream, oracle)
+    d = rb.states_to_device(base)
+    sums, hist = rb.consume(d, per_stream)
+    es = base.copy()
+    exp_sums, exp_hist = oracle.consume(es, per_stream)
+    assert (sums.cpu().numpy().view(np.uint64) == exp_sums).all()
+    assert (hist.cpu().numpy().view(np.uint32) == exp_hist).all()
+    assert rb.states_to_host(d).tobytes() == es.tobytes()
+
+
+def test_consume_flush_path(oracle):
+    # > 65535 rounds per lane forces the u16 private counters to flush
+    per = 32 * 65535 + 77
+    base = random_states(2, 5, oracle)
+    d = rb.states_to_device(base)
+    sums, hist = rb.consume(d, per)
+    es = base.copy()
+    exp_sums, exp_hist = oracle.consume(es, per)
+    assert (sums.cpu().numpy().view(np.uint64) == exp_sums).all()
+    assert (hist.cpu().numpy().view(np.uint32) == exp_hist).all()
+
+
+def test_config4_head(refvec):
+    c = refvec["c4_head"]
+    d = rb.make_streams(c["seed"], int(c["j"]), len(c["sums"]))
+    sums, hist = rb.consume(d, c["per_stream"])
+    assert sums.cpu().numpy().view(np.uint64).tolist() == c["sums"]
+    assert hist.cpu().numpy().view(np.uint32).tolist() == c["hist"]
+
+
+# -------------------------------------------------------------- K4 gaussian
+
+def ulp_diff(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    ia = a.view(np.int64)
+    ib = b.view(np.int64)
+    ia = np.where(ia < 0, np.int64(-0x8000000000000000) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-0x8000000000000000) - ib, ib)
+    return np.abs(ia - ib)
+
+
+def test_gaussian_within_one_ulp(oracle):
+    from oracle.bind import GAUSS_DTYPE
+    n, per, steps = 2000, 3, 100
+    states = rb.make_streams(7, 2**50, n)
+    g = rb.gauss_states_from(states)
+    out = rb.gaussian(g, per, steps).cpu().numpy()
+    og = np.zeros(n, GAUSS_DTYPE)
+    og["s"] = rb.states_to_host(states)
+    exp = oracle.gaussian_fill(og, per, steps)
+    d = ulp_diff(out.reshape(-1), exp.reshape(-1))
+    print(f"gaussian max ulp {d.max()}, differing {np.count_nonzero(d)} of {d.size}")
+    assert d.max() <= 1
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    assert gh["s"].tobytes() == og["s"].tobytes()
+    assert (gh["has_saved"] == og["has_saved"]).all()
+
+
+def test_gaussian_odd_count_keeps_cache(oracle):
+    from oracle.bind import GAUSS_DTYPE
+    states = rb.make_streams(7, 2**50, 64)
+    g = rb.gauss_states_from(states)
+    og = np.zeros(64, GAUSS_DTYPE)
+    og["s"] = rb.states_to_host(states)
+    for _ in range(3):  # 1 call per step: the cached deviate carries across launches
+        out = rb.gaussian(g, 1, 5).cpu().numpy()
+        exp = oracle.gaussian_fill(og, 1, 5)
+        assert ulp_diff(out.reshape(-1), exp.reshape(-1)).max() <= 1
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    assert (gh["has_saved"] == og["has_saved"]).all()
+
+
+# ------------------------------------------------------ invariants, host API
+
+def test_bad_state_is_flagged(oracle):
+    s = oracle.init(1)
+    s["j"] = 0  # separation != 64
+    d = rb.states_to_device(s)
+    rb.generate(d, 64, "u32")
+    torch.cuda.synchronize()
+    assert rb.device_status(clear=True) & 1
+
+
+def test_host_buffer_context(oracle):
+    ctx = rb.Context(0)
+    ss = ctx.make_streams(12345, 2**40, 300)
+    exp = oracle.make_streams(oracle.init(12345), 2**40, 300)
+    assert ss.tobytes() == exp.tobytes()
+    out = ctx.generate(ss, 1000, "f32")
+    eo = oracle.generate_f32(exp, 1000)
+    assert (out == eo).all() and ss.tobytes() == exp.tobytes()
+    h2d, d2h = ctx.traffic()
+    assert h2d == 300 * 400 and d2h == 300 * 1000 * 4 + 300 * 400
+    sums, hist = ctx.consume(ss, 4096)
+    es, eh = oracle.consume(exp, 4096)
+    assert (sums == es).all() and (hist == eh).all()
+    jumped = ctx.jump(ss, 2**120)
+    assert jumped[5:6].tobytes() == oracle.jump_state(exp[5:6], 2**120).tobytes()
+    with pytest.raises(ValueError):
+        ctx.make_streams(900000001, 5, 2)
+    ctx.close()
