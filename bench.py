@@ -59,6 +59,7 @@ class ClockSampler:
         self.t = None
 
     def __enter__(self):
+        self.started = time.perf_counter()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
@@ -158,7 +159,7 @@ def cpu_reference_c2(steps: int = 1, threads: int | None = None):
     host cores, on a bounded sample of config 2. Returns a dict or None."""
     from oracle.bind import Reference, reference_available
     threads = threads or os.cpu_count() or 1
-    n = int(min(C2["n"], 16384, 64 * threads))
+    n = int(min(C2["n"], 16384, 1024 * threads))
     out = np.empty(n * C2["per"], np.float32)
     if reference_available():
         ref, kind = Reference(), "reference"
@@ -233,23 +234,28 @@ def run_ours(args, rank, world, local):
             if ev:
                 ev[1].record(stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     gen_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = rb.kernel_launches()
-    barrier(world)
-    torch.cuda.synchronize()
+    # The clock sampler starts during warm-up (nvidia-smi needs ~0.3 s to emit)
+    # and stops right after the timed region, so every sample is under load.
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        while time.perf_counter() - clk.started < 0.5:
+            step()
+            torch.cuda.synchronize()
+        launches0 = rb.kernel_launches()
+        barrier(world)
+        torch.cuda.synchronize()
         t0.record(stream)
         for k in range(args.steps):
             step(gen_events[k])
         t1.record(stream)
         torch.cuda.synchronize()
+        launches = rb.kernel_launches() - launches0
     barrier(world)
-    launches = rb.kernel_launches() - launches0
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, world)
     gen_ms = statistics.mean(a.elapsed_time(b) for a, b in gen_events)
@@ -413,7 +419,7 @@ def run_ours(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--quick", action="store_true", help="config 2 only")

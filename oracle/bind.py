@@ -81,6 +81,7 @@ class Oracle:
             "or_generate_f32": (None, [vp, u64, u64, vp]),
             "or_consume": (None, [vp, u64, u64, vp, vp]),
             "or_gaussian_fill": (None, [vp, u64, u64, u64, vp]),
+            "or_glog": (C.c_double, [C.c_double]),
             "or_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
             "or_from_text": (i32, [C.c_char_p, vp]),
         }
@@ -179,11 +180,22 @@ class Oracle:
         self.lib.or_consume(_p(states), len(states), per_stream, _p(sums), _p(hist))
         return sums, hist
 
-    def gaussian_fill(self, gstates: np.ndarray, per_step: int, steps: int) -> np.ndarray:
+    def gaussian_fill(self, gstates: np.ndarray, per_step: int, steps: int,
+                      libm_log: bool = False) -> np.ndarray:
+        """The repo's gaussian() convention; libm_log=True swaps in glibc log()
+        (diagnostic only: how far the convention's log is from the platform's)."""
         gstates = np.ascontiguousarray(gstates)
         out = np.empty((steps, len(gstates), per_step), np.float64)
-        self.lib.or_gaussian_fill(_p(gstates), len(gstates), per_step, steps, _p(out))
+        flag = C.c_int.in_dll(self.lib, "or_gauss_use_libm_log")
+        flag.value = int(libm_log)
+        try:
+            self.lib.or_gaussian_fill(_p(gstates), len(gstates), per_step, steps, _p(out))
+        finally:
+            flag.value = 0
         return out
+
+    def glog(self, x: float) -> float:
+        return self.lib.or_glog(x)
 
     def to_text(self, state: np.ndarray) -> str:
         buf = C.create_string_buffer(4096)

@@ -370,10 +370,51 @@ void or_consume(or_state* states, uint64_t n_streams, uint64_t per_stream, uint6
     }
 }
 
+/* The gaussian convention's log(): a fixed sequence of IEEE operations
+ * (binary64 +, -, *, / and fused multiply-add, each correctly rounded) so the
+ * device can reproduce it bit for bit. x = 2^k m with m in (sqrt2/2, sqrt2],
+ * f = m - 1 (exact), s = f / (2 + f), log1p(f) = 2 atanh(s) with the Taylor
+ * series of atanh to s^21 (|s| <= 0.1716, truncation < 2^-60 relative), and
+ * k ln2 added as a 42-bit head (exact k * head) plus a tail. Accuracy ~1 ulp
+ * (the rounding of s dominates); x must be a positive normal double, which
+ * rsq in (0, 1) of the polar method always is (rsq >= 2^-46). */
+double or_glog(double x) {
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    int k = (int)((b >> 52) & 0x7FF) - 1023;
+    const uint64_t mb = (b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+    double m;
+    memcpy(&m, &mb, 8);
+    if (m > 0x1.6a09e667f3bcdp+0) { /* sqrt(2) */
+        m *= 0.5;
+        k += 1;
+    }
+    const double f = m - 1.0;
+    const double s = f / (2.0 + f);
+    const double z = s * s;
+    double p = 0x1.8618618618618p-5;     /* 1/21 */
+    p = fma(p, z, 0x1.af286bca1af28p-5); /* 1/19 */
+    p = fma(p, z, 0x1.e1e1e1e1e1e1ep-5); /* 1/17 */
+    p = fma(p, z, 0x1.1111111111111p-4); /* 1/15 */
+    p = fma(p, z, 0x1.3b13b13b13b14p-4); /* 1/13 */
+    p = fma(p, z, 0x1.745d1745d1746p-4); /* 1/11 */
+    p = fma(p, z, 0x1.c71c71c71c71cp-4); /* 1/9 */
+    p = fma(p, z, 0x1.2492492492492p-3); /* 1/7 */
+    p = fma(p, z, 0x1.999999999999ap-3); /* 1/5 */
+    p = fma(p, z, 0x1.5555555555555p-2); /* 1/3 */
+    const double t = s * z;
+    const double l1p = 2.0 * fma(t, p, s); /* 2 atanh(s) */
+    const double kd = (double)k;
+    return fma(kd, 0x1.62e42fefa3800p-1, fma(kd, 0x1.ef35793c76730p-45, l1p));
+}
+
+int or_gauss_use_libm_log = 0; /* diagnostic: 1 = glibc log() instead of or_glog */
+
 /* Repo-defined gaussian(): Marsaglia polar method on uniform() = next_f64
  * (core.hpp:70-72). Pair convention as in Numerical Recipes' gasdev: draw
  * v1 then v2 (each 2u-1), reject while rsq >= 1 or rsq == 0, return v2*fac
- * and cache v1*fac for the next call. NOT pinned to LAMMPS (absent here). */
+ * and cache v1*fac for the next call; log is or_glog above, every other
+ * operation a single IEEE binary64 operation. NOT pinned to LAMMPS (absent). */
 double or_gaussian(or_gauss_state* g) {
     if (g->has_saved) {
         g->has_saved = 0;
@@ -385,7 +426,8 @@ double or_gaussian(or_gauss_state* g) {
         v2 = 2.0 * ((double)or_step(&g->s) * 0x1p-24) - 1.0;
         rsq = v1 * v1 + v2 * v2;
     } while (rsq >= 1.0 || rsq == 0.0);
-    const double fac = sqrt(-2.0 * log(rsq) / rsq);
+    const double lg = or_gauss_use_libm_log ? log(rsq) : or_glog(rsq);
+    const double fac = sqrt(-2.0 * lg / rsq);
     g->saved = v1 * fac;
     g->has_saved = 1;
     return v2 * fac;

@@ -102,6 +102,8 @@ typedef struct or_gauss_state {
     uint32_t has_saved;
     uint32_t pad;
 } or_gauss_state;
+double or_glog(double x);
+extern int or_gauss_use_libm_log;
 double or_gaussian(or_gauss_state* g);
 void or_gaussian_fill(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step, uint64_t steps,
                       double* out /* [step][atom][per_step] */);

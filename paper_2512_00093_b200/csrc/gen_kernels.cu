@@ -208,6 +208,37 @@ __global__ void __launch_bounds__(32 * kConsumeWarps)
 // rsq >= 1 or rsq == 0, return v2 * fac and cache v1 * fac.
 constexpr int kGaussThreads = 128;
 
+// gaussian()'s log: the repo convention's fixed IEEE sequence (see
+// oracle/ranmar_oracle.c or_glog for the derivation), written with explicit
+// round-to-nearest intrinsics so nvcc cannot contract or reorder anything and
+// the device result is bit-identical to the CPU definition.
+__device__ __forceinline__ double glog(double x) {
+    const long long b = __double_as_longlong(x);
+    int k = static_cast<int>((b >> 52) & 0x7FF) - 1023;
+    double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+    if (m > 0x1.6a09e667f3bcdp+0) {
+        m = __dmul_rn(m, 0.5);
+        k += 1;
+    }
+    const double f = __dsub_rn(m, 1.0);
+    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+    const double z = __dmul_rn(s, s);
+    double p = 0x1.8618618618618p-5;
+    p = __fma_rn(p, z, 0x1.af286bca1af28p-5);
+    p = __fma_rn(p, z, 0x1.e1e1e1e1e1e1ep-5);
+    p = __fma_rn(p, z, 0x1.1111111111111p-4);
+    p = __fma_rn(p, z, 0x1.3b13b13b13b14p-4);
+    p = __fma_rn(p, z, 0x1.745d1745d1746p-4);
+    p = __fma_rn(p, z, 0x1.c71c71c71c71cp-4);
+    p = __fma_rn(p, z, 0x1.2492492492492p-3);
+    p = __fma_rn(p, z, 0x1.999999999999ap-3);
+    p = __fma_rn(p, z, 0x1.5555555555555p-2);
+    const double t = __dmul_rn(s, z);
+    const double l1p = __dmul_rn(2.0, __fma_rn(t, p, s));
+    const double kd = static_cast<double>(k);
+    return __fma_rn(kd, 0x1.62e42fefa3800p-1, __fma_rn(kd, 0x1.ef35793c76730p-45, l1p));
+}
+
 struct RingGen {
     uint32_t* ring;  // column base for this thread
     int i;           // cursor (j = i - 64 mod 97)
@@ -266,12 +297,12 @@ __global__ void __launch_bounds__(kGaussThreads)
                     g_out = saved;
                 } else {
                     double v1, v2, rsq;
-                    do {
-                        v1 = 2.0 * (static_cast<double>(gen.next()) * 0x1p-24) - 1.0;
-                        v2 = 2.0 * (static_cast<double>(gen.next()) * 0x1p-24) - 1.0;
-                        rsq = v1 * v1 + v2 * v2;  // exact: <= 48 significant bits
+                    do {  // v = 2u - 1 and rsq are exact in binary64 (<= 48 bits)
+                        v1 = __dsub_rn(__dmul_rn(static_cast<double>(gen.next()), 0x1p-23), 1.0);
+                        v2 = __dsub_rn(__dmul_rn(static_cast<double>(gen.next()), 0x1p-23), 1.0);
+                        rsq = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
                     } while (rsq >= 1.0 || rsq == 0.0);
-                    const double fac = sqrt(__ddiv_rn(-2.0 * log(rsq), rsq));
+                    const double fac = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glog(rsq)), rsq));
                     saved = __dmul_rn(v1, fac);
                     has = true;
                     g_out = __dmul_rn(v2, fac);

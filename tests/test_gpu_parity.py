@@ -262,7 +262,13 @@ def test_gaussian_within_one_ulp(oracle):
     exp = oracle.gaussian_fill(og, per, steps)
     d = ulp_diff(out.reshape(-1), exp.reshape(-1))
     print(f"gaussian max ulp {d.max()}, differing {np.count_nonzero(d)} of {d.size}")
-    assert d.max() <= 1
+    assert d.max() <= 1  # north-star tolerance; the shared log convention gives 0
+    og2 = np.zeros(n, GAUSS_DTYPE)
+    og2["s"] = rb.states_to_host(states)
+    libm = oracle.gaussian_fill(og2, per, steps, libm_log=True)
+    d2 = ulp_diff(out.reshape(-1), libm.reshape(-1))
+    print(f"vs a glibc-log() variant of the convention: max ulp {d2.max()}")
+    assert d2.max() <= 4
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
     assert gh["s"].tobytes() == og["s"].tobytes()
     assert (gh["has_saved"] == og["has_saved"]).all()

@@ -206,3 +206,22 @@ def test_live_reference_agrees(oracle, reference):
         assert oracle.jump_state(a, j).tobytes() == reference.jump_state(a, j).tobytes()
     with pytest.raises(ValueError):
         reference.init(900000001)
+
+
+def test_gaussian_log_convention_is_a_good_log(oracle):
+    # or_glog is part of the repo-defined gaussian() convention (no reference
+    # counterpart); it must be a faithful log on the polar method's domain.
+    import math
+    rng = random.Random(9)
+    worst = 0
+    for _ in range(20000):
+        n1, n2 = rng.randrange(-2**23, 2**23 + 1), rng.randrange(-2**23, 2**23 + 1)
+        rsq = (n1 * n1 + n2 * n2) / 2.0**46
+        if not 0 < rsq < 1:
+            continue
+        a, b = oracle.glog(rsq), math.log(rsq)
+        ia, ib = np.array([a]).view(np.int64)[0], np.array([b]).view(np.int64)[0]
+        worst = max(worst, abs(int(ia) - int(ib)))
+    assert worst <= 2
+    for x in (2.0**-46, 0.5, 0.999999999, 1e-10, 0.7071067811865476, 0.7071067811865475):
+        assert abs(oracle.glog(x) - math.log(x)) <= 2 * math.ulp(math.log(x))
