@@ -31,35 +31,41 @@ __device__ __forceinline__ int mod97(int64_t x) {
     return static_cast<int>(r < 0 ? r + 97 : r);
 }
 
-// Generic warp-per-stream driver. emit(round, raw, valid) is called once per
-// round per lane with raw = x_n - v_n (unmasked), n = 32 * round + lane.
-template <class Emit>
-__device__ __forceinline__ void warp_stream(ranmar_state* st, uint64_t N, uint32_t* status,
-                                            Emit&& emit) {
-    const int l = threadIdx.x & 31;
-    const int i0 = st->i, j0 = st->j;
-    const uint32_t v0 = st->v;
-    if (!state_ok(i0, j0, v0)) {
-        if (l == 0) atomicOr(status, kStatusBadState);
-        return;
+// Warp-per-stream generator: lane l of round r produces x_{32 r + l}.
+struct WarpGen {
+    uint32_t R1, R2, R3, R4;  // y[r-1..r-4][l]
+    uint32_t prev;            // lane 0's operand for the next round
+    uint32_t V;               // v of this lane's next output
+    uint32_t A32;             // 32 (m - d) mod m
+    int src, l, i0, j0;
+    uint32_t v0;
+
+    // Loads the state; false (and the status bit) if it violates the invariants.
+    __device__ __forceinline__ bool load(const ranmar_state* st, uint32_t* status) {
+        l = threadIdx.x & 31;
+        i0 = st->i;
+        j0 = st->j;
+        v0 = st->v;
+        if (!state_ok(i0, j0, v0)) {
+            if (l == 0) atomicOr(status, kStatusBadState);
+            return false;
+        }
+        // x_n = lane[(i0 - n) mod 97] for n in [-97, -1].
+        const uint32_t* lane = st->lane;
+        R1 = lane[(i0 + 32 - l) % 97];
+        R2 = lane[(i0 + 64 - l) % 97];
+        R3 = lane[(i0 + 96 - l) % 97];
+        R4 = (l == 31) ? lane[i0] : 0u;  // x_{-97}; other lanes' round -4 is never read
+        src = (l + 31) & 31;
+        // Lane 0's operand for round 0 is lane 31's (x_{-97} - x_{-33}).
+        prev = __shfl_sync(0xffffffffu, R4 - R2, src);
+        V = arith_advance(v0, static_cast<uint64_t>(l) + 1);
+        A32 = static_cast<uint32_t>((32ull * kStepA) % kMod);
+        return true;
     }
-    // x_n = lane[(i0 - n) mod 97] for n in [-97, -1].
-    const uint32_t* lane = st->lane;
-    uint32_t R1 = lane[(i0 + 32 - l) % 97];
-    uint32_t R2 = lane[(i0 + 64 - l) % 97];
-    uint32_t R3 = lane[(i0 + 96 - l) % 97];
-    uint32_t R4 = (l == 31) ? lane[i0] : 0u;  // x_{-97}; other lanes' round -4 is never used
-    // Lane 0's operand for round 0 is lane 31's (x_{-97} - x_{-33}).
-    uint32_t prev = __shfl_sync(0xffffffffu, R4 - R2, (l + 31) & 31);
-    uint32_t V = arith_advance(v0, static_cast<uint64_t>(l) + 1);
-    const uint32_t A32 = static_cast<uint32_t>((32ull * kStepA) % kMod);
 
-    const uint64_t full = N >> 5;
-    const uint32_t tail = static_cast<uint32_t>(N & 31);
-    const int src = (l + 31) & 31;
-
-#pragma unroll 4
-    for (uint64_t r = 0; r < full; ++r) {
+    // One round: returns x_n - v_n (unmasked) for n = 32 r + l.
+    __device__ __forceinline__ uint32_t round() {
         const uint32_t S = __shfl_sync(0xffffffffu, R3 - R1, src);
         const uint32_t y = (l == 0) ? prev : S;
         prev = S;
@@ -67,35 +73,43 @@ __device__ __forceinline__ void warp_stream(ranmar_state* st, uint64_t N, uint32
         R3 = R2;
         R2 = R1;
         R1 = y;
-        emit(r, y - V, true);
+        const uint32_t raw = y - V;
         V = add_mod_m(V, A32);
+        return raw;
     }
-    uint64_t rounds = full;
-    if (tail) {
-        const uint32_t S = __shfl_sync(0xffffffffu, R3 - R1, src);
-        const uint32_t y = (l == 0) ? prev : S;
-        R4 = R3;
-        R3 = R2;
-        R2 = R1;
-        R1 = y;
-        emit(full, y - V, static_cast<uint32_t>(l) < tail);
-        rounds = full + 1;
-    }
-    __syncwarp();
-    // Write back the ring: registers R_k hold round (rounds - k).
-    uint32_t* lane_w = st->lane;
-    const int64_t lo = static_cast<int64_t>(N) - 97, hi = static_cast<int64_t>(N);
-    const uint32_t regs[4] = {R1, R2, R3, R4};
+
+    // Writes the state N = per-stream outputs later, exactly as N step()
+    // calls leave it; `rounds` = rounds executed (ceil(N / 32)).
+    __device__ __forceinline__ void store(ranmar_state* st, uint64_t N, uint64_t rounds) {
+        __syncwarp();
+        uint32_t* lane_w = st->lane;
+        const int64_t lo = static_cast<int64_t>(N) - 97, hi = static_cast<int64_t>(N);
+        const uint32_t regs[4] = {R1, R2, R3, R4};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t n = 32 * (static_cast<int64_t>(rounds) - 1 - k) + l;
-        if (n >= lo && n < hi) lane_w[mod97(static_cast<int64_t>(i0) - n)] = regs[k] & kMask;
+        for (int k = 0; k < 4; ++k) {
+            const int64_t n = 32 * (static_cast<int64_t>(rounds) - 1 - k) + l;
+            if (n >= lo && n < hi) lane_w[mod97(static_cast<int64_t>(i0) - n)] = regs[k] & kMask;
+        }
+        if (l == 0) {
+            st->i = mod97(static_cast<int64_t>(i0) - static_cast<int64_t>(N % 97));
+            st->j = mod97(static_cast<int64_t>(j0) - static_cast<int64_t>(N % 97));
+            st->v = arith_advance(v0, N);
+        }
     }
-    if (l == 0) {
-        st->i = mod97(static_cast<int64_t>(i0) - static_cast<int64_t>(N % 97));
-        st->j = mod97(static_cast<int64_t>(j0) - static_cast<int64_t>(N % 97));
-        st->v = arith_advance(v0, N);
-    }
+};
+
+// Drives a WarpGen over N outputs: emit(r, raw, valid) per round.
+template <class Emit>
+__device__ __forceinline__ void warp_stream(ranmar_state* st, uint64_t N, uint32_t* status,
+                                            Emit&& emit) {
+    WarpGen g;
+    if (!g.load(st, status)) return;
+    const uint64_t full = N >> 5;
+    const uint32_t tail = static_cast<uint32_t>(N & 31);
+#pragma unroll 4
+    for (uint64_t r = 0; r < full; ++r) emit(r, g.round(), true);
+    if (tail) emit(full, g.round(), static_cast<uint32_t>(g.l) < tail);
+    g.store(st, N, full + (tail ? 1 : 0));
 }
 
 template <class T>
@@ -159,6 +173,16 @@ __device__ __forceinline__ void flush_hist(uint32_t* hw, uint32_t* __restrict__ 
     __syncwarp();
 }
 
+// Histogram update for one output u (24-bit): byte offset of bin u >> 16 in
+// this lane's column, ((bin >> 1) * 32 words) * 4 + (bin & 1) * 2.
+__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u) {
+    // hb: 32-bit shared-window address of this lane's column
+    const uint32_t a = hb + (((u >> 10) & 0x3F80u) | ((u >> 15) & 2u));
+    uint32_t c;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(a));
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(c + 1) : "memory");
+}
+
 __global__ void __launch_bounds__(32 * kConsumeWarps)
     consume_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
                    uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status) {
@@ -169,32 +193,46 @@ __global__ void __launch_bounds__(32 * kConsumeWarps)
     uint32_t* hw = smem_hist + w * kHistWordsPerWarp;
     for (uint32_t i = l; i < kHistWordsPerWarp; i += 32) hw[i] = 0;
     __syncwarp();
-    unsigned char* hb = reinterpret_cast<unsigned char*>(hw) + 4 * l;
+    const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hw)) + 4 * l;
     uint32_t* gh = hist + k * 256;
 
+    WarpGen g;
+    if (!g.load(states + k, status)) return;
+    const uint64_t N = per_stream, full = N >> 5;
+    const uint32_t tail = static_cast<uint32_t>(N & 31);
     uint64_t sum64 = 0;
-    uint32_t sum32 = 0;
     bool flushed = false;
-    warp_stream(states + k, per_stream, status, [&](uint64_t r, uint32_t raw, bool valid) {
-        if (valid) {
-            const uint32_t u = raw & kMask;
-            sum32 += u;
-            // byte offset of (bin = u >> 16): ((bin >> 1) * 32 words) * 4 + (bin & 1) * 2
-            const uint32_t off = ((u >> 10) & 0x3F80u) | ((u >> 15) & 2u);
-            unsigned short* c = reinterpret_cast<unsigned short*>(hb + off);
-            *c = static_cast<unsigned short>(*c + 1);
+    uint64_t r = 0;
+    while (r < full) {
+        // <= kFlushRounds rounds between flushes (u16 counters), sums in
+        // blocks of <= 128 rounds (128 x 24-bit values fit 32 bits).
+        const uint64_t chunk_end = min(full, r + kFlushRounds);
+        while (r < chunk_end) {
+            const uint64_t left = chunk_end - r;
+            const uint32_t blk = left < 128 ? static_cast<uint32_t>(left) : 128u;
+            uint32_t s32 = 0;
+#pragma unroll 4
+            for (uint32_t q = 0; q < blk; ++q) {
+                const uint32_t u = g.round() & kMask;
+                s32 += u;
+                hist_add(hb, u);
+            }
+            sum64 += s32;
+            r += blk;
         }
-        if ((r & 127) == 127) {  // 128 x 24-bit values fit 32 bits
-            sum64 += sum32;
-            sum32 = 0;
-        }
-        if (r % kFlushRounds == kFlushRounds - 1) {
+        if (r < full || tail) {
             flush_hist(hw, gh, true, flushed);
             flushed = true;
         }
-    });
-    sum64 += sum32;
-    // Warp-reduce the lane sums.
+    }
+    if (tail) {
+        const uint32_t u = g.round() & kMask;
+        if (static_cast<uint32_t>(l) < tail) {
+            sum64 += u;
+            hist_add(hb, u);
+        }
+    }
+    g.store(states + k, N, full + (tail ? 1 : 0));
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum64 += __shfl_xor_sync(0xffffffffu, sum64, o);
     if (l == 0) sums[k] = sum64;

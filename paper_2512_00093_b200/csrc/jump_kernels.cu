@@ -8,24 +8,28 @@
 // without changing a single residue. Tensor cores are not used: this is
 // modular integer arithmetic, not a float contraction.
 //
-//  pow_kernel        K3a  t^E mod phi by left-to-right square-and-multiply in
-//                         shared memory (one CTA per exponent), symmetric
-//                         squaring (4,753 MACs instead of 9,409) and the
-//                         trinomial fold split into three conflict-free phases
-//                         (sources [160,192], [127,159], [97,126]); optional
-//                         chain of further squarings P_{2^b E}.
-//  mulmod_kernel          batched products a_r * Q mod phi (warp per product);
-//                         builds the offset table T_r = P_{rJ} by doubling.
+//  pow_kernel        K3a  the squaring chain t^(2^k) mod phi in shared memory
+//                         (one CTA): symmetric squaring (4,753 MACs instead of
+//                         9,409) and the trinomial fold split into three
+//                         conflict-free phases (sources [160,192], [127,159],
+//                         [97,126]). Run once per device to fill the square
+//                         table Z_k = t^(2^k), k < 320.
+//  pow_table_kernel  K3a  the multiply half: t^(E 2^s) = prod_{k in bits(E)}
+//                         Z_{k+s} (right-to-left square-and-multiply with the
+//                         cached squares), one CTA per exponent, warps reduce
+//                         strided factor subsets then a tree.
+//  tables_kernel          offset tables Tab_L[r] = P_{r 128^L J}, r < 128.
 //  apply_kernel      K3b  u * P(A) for a batch of states as a Hankel product
-//                         out[m] = sum_j p_j w[j + m] over the 208-term
-//                         recurrence extension w of u (no sequential Horner
-//                         chain), + K3c the closed-form arithmetic jump.
-//  bulk_kernel       K3b  make_streams' stream starts s_{(first + 128h + r)J}
-//                         = apply(anchor_h, T_r): per anchor a 128 x 104 x 104
-//                         integer "GEMM" tile with a 4 x 8 register tile per
-//                         thread; T^T stays in shared memory for all anchors
-//                         a CTA visits, results are staged and written as
-//                         contiguous 400-B state records.
+//                         out[m] = sum_j p_j w[j + m] over the recurrence
+//                         extension w of u (no sequential Horner chain), + K3c
+//                         the closed-form arithmetic jump.
+//  level_kernel      K3b  one level of the base-128 stream-start tree
+//                         S_L[k] = apply(S_{L+1}[k / 128], Tab_L[k % 128]).
+//  bulk_kernel       K3b  level 0 (all stream starts): per anchor a 128 x 97
+//                         x 97 integer "GEMM" tile on the IMAD pipe, T^T
+//                         resident in shared memory, double-buffered anchor
+//                         extensions, 4 x 8 register tiles, results stored
+//                         from registers as 16-B vectors.
 #include <cstdint>
 
 #include "ranmar_device.cuh"
@@ -33,8 +37,6 @@
 namespace rb {
 
 constexpr int kPolyN = 97;
-constexpr int kWExt = 208;   // recurrence-extension length used by the Hankel products
-constexpr int kJPad = 104;   // coefficients padded to 13 x 8
 constexpr int kRows = 128;   // offsets per anchor (T table rows)
 
 struct PowJob {
@@ -130,61 +132,130 @@ __global__ void __launch_bounds__(kPowThreads) pow_kernel(PowJobs jobs) {
     }
 }
 
-// ---- T table: T_0 = 1, T_{r + half} = T_r * Q for r < half (warp per product)
-constexpr int kMulWarps = 4;
-
-__global__ void __launch_bounds__(32 * kMulWarps)
-    mulmod_kernel(uint32_t* __restrict__ T, int half, int count, const uint32_t* __restrict__ Q) {
-    __shared__ uint32_t q[kPolyN];
-    __shared__ uint32_t as[kMulWarps][kPolyN];
-    __shared__ uint32_t cs[kMulWarps][193];
-    for (int k = threadIdx.x; k < kPolyN; k += blockDim.x) q[k] = Q[k];
-    __syncthreads();
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int r = blockIdx.x * kMulWarps + w;
-    if (r >= count) return;
-    uint32_t* a = as[w];
-    uint32_t* c = cs[w];
-    for (int k = l; k < kPolyN; k += 32) a[k] = T[r * kPolyN + k];
-    __syncwarp();
+// ---- warp-level product mod phi: out = a * b (a, b, out in shared memory,
+// out may alias a; c is a 193-word scratch). 9,409 MACs, then the fold.
+__device__ __forceinline__ void warp_mulmod(const uint32_t* a, const uint32_t* b, uint32_t* c,
+                                            uint32_t* out, int l) {
     for (int k = l; k < 193; k += 32) {
         const int lo = k > 96 ? k - 96 : 0, hi = k < 96 ? k : 96;
         uint32_t acc = 0;
-        for (int i = lo; i <= hi; ++i) acc += a[i] * q[k - i];
+        for (int i = lo; i <= hi; ++i) acc += a[i] * b[k - i];
         c[k] = acc;
     }
     __syncwarp();
-    fold_to(c, a, l, 32, [] { __syncwarp(); });
-    for (int k = l; k < kPolyN; k += 32) T[(r + half) * kPolyN + k] = a[k];
+    fold_to(c, out, l, 32, [] { __syncwarp(); });
 }
 
-__global__ void t_init_kernel(uint32_t* __restrict__ T) {
-    for (int k = threadIdx.x; k < kPolyN; k += blockDim.x) T[k] = (k == 0);
+__device__ __forceinline__ void warp_load_poly(uint32_t* dst, const uint32_t* src, int l) {
+    for (int k = l; k < kPolyN; k += 32) dst[k] = src[k];
+    __syncwarp();
 }
 
-// Tt[j][r] = T_r[j] (j < 97), 0 for j in [97, 104).
-__global__ void t_transpose_kernel(const uint32_t* __restrict__ T, uint32_t* __restrict__ Tt) {
-    const int r = threadIdx.x;  // 128 threads
-    for (int j = blockIdx.x; j < kJPad; j += gridDim.x)
-        Tt[j * kRows + r] = j < kPolyN ? T[r * kPolyN + j] : 0u;
+// ---- K3a from the cached squares: t^(E * 2^shift) = prod_{k in bits(E)} Z_{k+shift},
+// Z_k = t^(2^k) mod phi (right-to-left square-and-multiply; the squarings are
+// the per-device table, built once by pow_kernel). One CTA per job; each warp
+// multiplies a strided subset of the factors, then a 3-level tree.
+constexpr int kPowTabWarps = 8;
+constexpr int kMaxPowJobs = 64;
+
+struct PowTabJob {
+    uint64_t e[4];
+    int shift;
+    uint32_t* out;
+};
+struct PowTabJobs {
+    PowTabJob job[kMaxPowJobs];
+};
+
+__global__ void __launch_bounds__(32 * kPowTabWarps)
+    pow_table_kernel(const __grid_constant__ PowTabJobs jobs, const uint32_t* __restrict__ Z) {
+    __shared__ uint32_t acc[kPowTabWarps][kPolyN];
+    __shared__ uint32_t fac[kPowTabWarps][kPolyN];
+    __shared__ uint32_t scr[kPowTabWarps][193];
+    __shared__ int used[kPowTabWarps];
+    const PowTabJob& job = jobs.job[blockIdx.x];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int rank = 0;
+    bool have = false;
+    for (int k = 0; k < 256; ++k) {
+        if (!((job.e[k >> 6] >> (k & 63)) & 1u)) continue;
+        if (rank++ % kPowTabWarps != w) continue;
+        const uint32_t* zk = Z + static_cast<size_t>(k + job.shift) * kPolyN;
+        if (!have) {
+            warp_load_poly(acc[w], zk, l);
+            have = true;
+        } else {
+            warp_load_poly(fac[w], zk, l);
+            warp_mulmod(acc[w], fac[w], scr[w], acc[w], l);
+        }
+    }
+    if (l == 0) used[w] = have;
+    __syncthreads();
+    for (int stride = 1; stride < kPowTabWarps; stride *= 2) {
+        if (w % (2 * stride) == 0 && used[w + stride]) {
+            if (used[w]) {
+                warp_mulmod(acc[w], acc[w + stride], scr[w], acc[w], l);
+            } else {
+                warp_load_poly(acc[w], acc[w + stride], l);
+            }
+        }
+        __syncthreads();
+        if (w % (2 * stride) == 0 && l == 0) used[w] = used[w] | used[w + stride];
+        __syncthreads();
+    }
+    if (w == 0)
+        for (int k = l; k < kPolyN; k += 32) job.out[k] = used[0] ? acc[0][k] : (k == 0);
 }
 
-// ---- recurrence extension w[0..207] of a state's canonical vector
-// (canonicalize, jump.hpp:32-37; recurrence_extend, test_util.hpp:38-46).
-// Phases of <= 33 new terms: w[n] depends on w[n-97], w[n-33] only.
-template <class Sync>
-__device__ __forceinline__ void extend(uint32_t* W, int t, int nt, Sync sync) {
-    for (int p = 0; p < 4; ++p) {
-        const int lo = 97 + 33 * p, hi = min(lo + 33, kWExt);
-        for (int n = lo + t; n < hi; n += nt) W[n] = W[n - 97] - W[n - 33];
-        sync();
+// ---- offset tables: Tab_L[r] = P_{r 128^L J} = prod_{b in bits(r)} Q_{7L + b}
+// (warp per entry); Tab_0 also written transposed for the bulk kernel.
+constexpr int kTabWarps = 4;
+
+__global__ void __launch_bounds__(32 * kTabWarps)
+    tables_kernel(const uint32_t* __restrict__ Q, int levels, uint32_t* __restrict__ Tab,
+                  uint32_t* __restrict__ Tt) {
+    __shared__ uint32_t acc[kTabWarps][kPolyN];
+    __shared__ uint32_t fac[kTabWarps][kPolyN];
+    __shared__ uint32_t scr[kTabWarps][193];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int gw = blockIdx.x * kTabWarps + w;
+    if (gw >= levels * kRows) return;
+    const int lvl = gw / kRows, r = gw % kRows;
+    for (int k = l; k < kPolyN; k += 32) acc[w][k] = (k == 0);
+    __syncwarp();
+    for (int b = 0; b < 7; ++b) {
+        if (!((r >> b) & 1)) continue;
+        warp_load_poly(fac[w], Q + static_cast<size_t>(7 * lvl + b) * kPolyN, l);
+        warp_mulmod(acc[w], fac[w], scr[w], acc[w], l);
+    }
+    for (int k = l; k < kPolyN; k += 32) {
+        Tab[static_cast<size_t>(gw) * kPolyN + k] = acc[w][k];
+        if (lvl == 0) Tt[k * kRows + r] = acc[w][k];
+    }
+}
+
+// ---- recurrence extension of canonical vectors held in shared memory:
+// w[n] = w[n-97] - w[n-33] (test_util.hpp:38-46), phases of <= 33 terms.
+__device__ __forceinline__ void extend_items(uint32_t* W, int stride, int items, int len, int t,
+                                             int nt) {
+    for (int lo = 97; lo < len; lo += 33) {
+        const int cnt = min(33, len - lo);
+        for (int x = t; x < items * cnt; x += nt) {
+            const int it = x / cnt, n = lo + (x - it * cnt);
+            uint32_t* Wi = W + it * stride;
+            Wi[n] = Wi[n - 97] - Wi[n - 33];
+        }
+        __syncthreads();
     }
 }
 
 // ---- K3b/K3c for a batch: out[k] = jump(in[k]) with one shared P and dec.
+// (ranmar_jump_dev and the first anchor of make_streams.)
 constexpr int kApplyItems = 8;
 constexpr int kApplyThreads = kApplyItems * 13;  // 104: (item, column group of 8)
+constexpr int kWExt = 208;
 constexpr int kWStride = kWExt + 1;               // odd stride spreads banks
+constexpr int kJPad = 104;                        // coefficients padded to 13 x 8
 
 __global__ void __launch_bounds__(kApplyThreads)
     apply_kernel(const ranmar_state* in, ranmar_state* out, uint64_t n,
@@ -207,15 +278,7 @@ __global__ void __launch_bounds__(kApplyThreads)
         W[it * kWStride + kk] = in[k0 + it].lane[(iin[it] - kk + 97) % 97];
     }
     __syncthreads();
-    for (int ph = 0; ph < 4; ++ph) {  // extend() for all items at once, phase by phase
-        const int lo = 97 + 33 * ph, len = min(33, kWExt - lo);
-        for (int x = t; x < items * len; x += kApplyThreads) {
-            const int it = x / len, n = lo + (x - it * len);
-            uint32_t* Wi = W + it * kWStride;
-            Wi[n] = Wi[n - 97] - Wi[n - 33];
-        }
-        __syncthreads();
-    }
+    extend_items(W, kWStride, items, kWExt, t, kApplyThreads);
 
     const int it = t / 13, cg = t - it * 13;
     if (it < items) {
@@ -251,21 +314,119 @@ __global__ void __launch_bounds__(kApplyThreads)
     }
 }
 
+// ---- one level of the base-128 stream-start tree:
+//   S_L[k] = apply(S_{L+1}[k / 128], Tab_L[k % 128]),  k < count
+// (the arithmetic part by jump_arith with (k % 128) * 128^L * J). WMODE
+// writes the 193-term canonical extension + v (what the bulk kernel reads)
+// instead of a decanonicalized state.
+constexpr int kWAnchor = 196;  // words per anchor extension row (193 used)
+
+template <bool WMODE>
+__global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13))
+    level_kernel(const ranmar_state* __restrict__ in, uint64_t count,
+                 const uint32_t* __restrict__ Tab, uint32_t c_lvl, ranmar_state* __restrict__ out,
+                 uint32_t* __restrict__ outW, uint32_t* __restrict__ outV) {
+    constexpr int CG = WMODE ? 25 : 13;          // column groups of 8
+    constexpr int NT = kApplyItems * CG;
+    constexpr int EXT = 97 + 8 * CG;             // 297 / 201
+    constexpr int STR = (EXT + 8) | 1;           // odd stride
+    __shared__ uint32_t W[kApplyItems * STR];
+    __shared__ uint32_t p[kApplyItems][kJPad];
+    __shared__ uint32_t vin[kApplyItems];
+    __shared__ int iin[kApplyItems];
+    const int t = threadIdx.x;
+    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kApplyItems;
+    const int items = static_cast<int>(count - k0 < (uint64_t)kApplyItems ? count - k0 : (uint64_t)kApplyItems);
+    for (int x = t; x < items * kJPad; x += NT) {
+        const int it = x / kJPad, j = x - it * kJPad;
+        p[it][j] = j < kPolyN ? Tab[((k0 + it) % kRows) * kPolyN + j] : 0u;
+    }
+    if (t < items) {
+        const ranmar_state* s = in + (k0 + t) / kRows;
+        iin[t] = s->i;
+        vin[t] = s->v;
+    }
+    __syncthreads();
+    for (int x = t; x < items * kPolyN; x += NT) {
+        const int it = x / kPolyN, kk = x - it * kPolyN;
+        W[it * STR + kk] = in[(k0 + it) / kRows].lane[(iin[it] - kk + 97) % 97];
+    }
+    __syncthreads();
+    extend_items(W, STR, items, EXT + 8, t, NT);
+
+    const int it = t / CG, cg = t - it * CG;
+    if (it >= items) return;
+    const uint32_t* w_it = W + it * STR + 8 * cg;
+    const uint32_t* p_it = p[it];
+    uint32_t acc[8], win[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        acc[c] = 0;
+        win[c] = w_it[c];
+    }
+#pragma unroll 1
+    for (int j0 = 0; j0 < kJPad; j0 += 8) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const uint32_t pj = p_it[j0 + jj];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] += pj * win[(jj + c) & 7];
+            win[jj] = w_it[j0 + jj + 8];
+        }
+    }
+    const uint64_t k = k0 + it;
+    const uint64_t r = k % kRows;
+    const uint32_t dec = static_cast<uint32_t>((r * c_lvl % kMod) * kDelta % kMod);
+    const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(vin[it]) + (kMod - dec)) % kMod);
+    if (WMODE) {
+        uint32_t* o = outW + k * kWAnchor;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int m = 8 * cg + c;
+            if (m < 193) o[m] = acc[c] & kMask;
+        }
+        if (cg == 0) outV[k] = v;
+    } else {
+        ranmar_state* o = out + k;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int m = 8 * cg + c;
+            if (m < kPolyN) o->lane[96 - m] = acc[c] & kMask;
+        }
+        if (cg == 0) {
+            o->i = 96;
+            o->j = 32;
+            o->v = v;
+        }
+    }
+}
+
 __global__ void put_state_kernel(ranmar_state s, ranmar_state* dst) {
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     const uint32_t* src = reinterpret_cast<const uint32_t*>(&s);
     for (int k = threadIdx.x; k < 100; k += blockDim.x) d[k] = src[k];
 }
 
-// ---- make_streams bulk: s_{(first + 128 h + r) J} = apply(anchor_h, T_r)
-constexpr int kBulkThreads = 13 * 32;  // warp = column group (8 columns), lane = 4 rows
-constexpr int kStageWords = kRows * 100;
-constexpr size_t kBulkSmem = (kJPad * kRows + kWExt + kStageWords + 8) * 4;
+// ---- make_streams bulk (level 0): s_{(first + 128 h + r) J} = apply(anchor_h, T_r).
+// Per anchor a 128 x 97 x 97 integer "GEMM" tile on the IMAD pipe:
+//  * T^T (97 x 128) stays in shared memory for every anchor the CTA visits;
+//  * the anchor's 193-term extension is prefetched into the other half of a
+//    double buffer while the current one is consumed (one barrier per anchor);
+//  * warp g owns state words [8g, 8g + 8) (columns m = 89 - 8g .. 96 - 8g of
+//    the canonical vector, reversed by decanonicalize), lane rg owns rows
+//    4rg .. 4rg + 3: a 4 x 8 register tile, one LDS.128 of T and one sliding
+//    LDS of the extension per j for 32 IMADs;
+//  * warps 0-3 add column m = 0 (state word 96) for one row per lane and
+//    write the record tail (lane[96], i, j, v) as one 16-B store;
+//  * results go straight from registers to HBM as 16-B stores (no staging).
+constexpr int kBulkWarps = 12;
+constexpr int kBulkThreads = 32 * kBulkWarps;
+constexpr size_t kBulkSmem = (size_t(kPolyN) * kRows + 2 * kWAnchor) * 4;
 
 struct BulkArgs {
-    const ranmar_state* anchors;
-    uint64_t H;           // anchors
-    const uint32_t* Tt;   // [104][128]
+    const uint32_t* W1;   // anchors' extensions, H x kWAnchor
+    uint64_t H;
+    const uint32_t* Tt;   // [97][128]
     ranmar_state* out;    // streams [first, first + n)
     uint64_t first, n;
     uint32_t v_base;      // v of the base state
@@ -274,40 +435,37 @@ struct BulkArgs {
 };
 
 __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_constant__ BulkArgs args) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* Tt = sm;                       // [104][128]
-    uint32_t* W = Tt + kJPad * kRows;        // [208]
-    uint32_t* stage = W + kWExt;             // [128][100] state records
-    int* anchor_i = reinterpret_cast<int*>(stage + kStageWords);
+    extern __shared__ uint4 sm4[];
+    uint32_t* Tt = reinterpret_cast<uint32_t*>(sm4);  // [97][128]
+    uint32_t* Wb = Tt + kPolyN * kRows;               // [2][196]
     const int t = threadIdx.x;
-    const int cg = t >> 5, rg = t & 31;
+    const int g = t >> 5, rg = t & 31;
+    const int m0 = 89 - 8 * g;
 
-    {   // T^T tile, loaded once per CTA (vectorised)
+    {   // T^T tile, loaded once per CTA
         const uint4* src = reinterpret_cast<const uint4*>(args.Tt);
-        uint4* dst = reinterpret_cast<uint4*>(Tt);
-        for (int x = t; x < kJPad * kRows / 4; x += kBulkThreads) dst[x] = src[x];
+        for (int x = t; x < kPolyN * kRows / 4; x += kBulkThreads) sm4[x] = src[x];
     }
+    uint64_t h = blockIdx.x;
+    if (h < args.H && t < 193) Wb[t] = args.W1[h * kWAnchor + t];
+    __syncthreads();
 
-    for (uint64_t h = blockIdx.x; h < args.H; h += gridDim.x) {
-        const ranmar_state* A = args.anchors + h;
-        if (t == 0) *anchor_i = A->i;
-        __syncthreads();
-        const int ai = *anchor_i;
-        for (int kk = t; kk < kPolyN; kk += kBulkThreads) W[kk] = A->lane[(ai - kk + 97) % 97];
-        __syncthreads();
-        extend(W, t, kBulkThreads, [] { __syncthreads(); });
+    for (int it = 0; h < args.H; ++it, h += gridDim.x) {
+        const uint32_t* W = Wb + (it & 1) * kWAnchor;
+        const uint64_t hn = h + gridDim.x;
+        if (hn < args.H && t < 193) Wb[((it + 1) & 1) * kWAnchor + t] = args.W1[hn * kWAnchor + t];
 
         uint32_t acc[4][8];
         uint32_t win[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            win[c] = W[8 * cg + c];
+            win[c] = W[m0 + c];
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) acc[rr][c] = 0;
         }
-        const uint32_t* wcg = W + 8 * cg;
+        const uint32_t* wcg = W + m0;
 #pragma unroll 1
-        for (int j0 = 0; j0 < kJPad; j0 += 8) {
+        for (int j0 = 0; j0 < 96; j0 += 8) {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
                 const uint4 tv = *reinterpret_cast<const uint4*>(Tt + (j0 + jj) * kRows + 4 * rg);
@@ -319,36 +477,43 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
                 win[jj] = wcg[j0 + jj + 8];
             }
         }
-        // Stage decanonicalized records: lane[96 - m] = out[m] (jump.hpp:42-48).
+        {   // j = 96: slot c holds W[96 + m0 + c]
+            const uint4 tv = *reinterpret_cast<const uint4*>(Tt + 96 * kRows + 4 * rg);
+            const uint32_t tr[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[rr][c] += tr[rr] * win[c];
+        }
+        const uint64_t row0 = h * kRows;
+        const uint64_t rows = args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows;
+        const bool skip0 = args.first == 0 && h == 0;  // stream 0 is the base itself
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
-            uint32_t* rec = stage + (4 * rg + rr) * 100;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int m = 8 * cg + c;
-                if (m < kPolyN) rec[96 - m] = acc[rr][c] & kMask;
+            const uint64_t row = 4 * rg + rr;
+            if (row >= rows || (skip0 && row == 0)) continue;
+            uint4* dst = reinterpret_cast<uint4*>(args.out[row0 + row].lane + 8 * g);
+            // word 8g + q holds canonical column 96 - 8g - q = m0 + 7 - q
+            dst[0] = make_uint4(acc[rr][7] & kMask, acc[rr][6] & kMask, acc[rr][5] & kMask,
+                                acc[rr][4] & kMask);
+            dst[1] = make_uint4(acc[rr][3] & kMask, acc[rr][2] & kMask, acc[rr][1] & kMask,
+                                acc[rr][0] & kMask);
+        }
+        if (g < 4) {  // column m = 0 -> state word 96, plus i, j, v
+            const int row = 32 * g + rg;
+            uint32_t a0 = 0;
+#pragma unroll 8
+            for (int j = 0; j < kPolyN; ++j) a0 += Tt[j * kRows + row] * W[j];
+            if (static_cast<uint64_t>(row) < rows && !(skip0 && row == 0)) {
+                const uint64_t k = args.first + row0 + row;
+                const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
+                const uint32_t v = static_cast<uint32_t>((args.v_base + (kMod - dec)) % kMod);
+                *reinterpret_cast<uint4*>(args.out[row0 + row].lane + 96) =
+                    make_uint4(a0 & kMask, 96u, 32u, v);
             }
         }
-        if (t < kRows) {
-            const uint64_t k = args.first + h * kRows + t;  // global stream index
-            uint32_t* rec = stage + t * 100;
-            rec[97] = 96;
-            rec[98] = 32;
-            // jump_arith(v_base, k J) (jump.hpp:79-86): (k J) mod m = (k mod m)(J mod m) mod m
-            const uint64_t km = (k % kMod) * args.jm % kMod;
-            const uint64_t dec = km * kDelta % kMod;
-            rec[99] = static_cast<uint32_t>((args.v_base + (kMod - dec)) % kMod);
-        }
-        __syncthreads();
-        const uint64_t row0 = h * kRows;
-        if (args.first == 0 && row0 == 0) {  // stream 0 is the base itself (jump.hpp:116)
-            if (t < 100) stage[t] = reinterpret_cast<const uint32_t*>(&args.base)[t];
-            __syncthreads();
-        }
-        const int rows = static_cast<int>(args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows);
-        uint4* dst = reinterpret_cast<uint4*>(args.out + row0);
-        const uint4* srcv = reinterpret_cast<const uint4*>(stage);
-        for (int x = t; x < rows * 25; x += kBulkThreads) dst[x] = srcv[x];
+        if (skip0 && t < 100)
+            reinterpret_cast<uint32_t*>(args.out)[t] = reinterpret_cast<const uint32_t*>(&args.base)[t];
         __syncthreads();
     }
 }
@@ -363,17 +528,29 @@ cudaError_t launch_pow(const PowJobs& jobs, int njobs, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_t_table(uint32_t* T, uint32_t* Tt, const uint32_t* Q, cudaStream_t stream) {
-    count_launch();
-    t_init_kernel<<<1, 128, 0, stream>>>(T);
-    for (int b = 0; (1 << b) < kRows; ++b) {
-        const int half = 1 << b;
+// jobs: (exponent, shift, out) triples; Z: the per-device square table.
+cudaError_t launch_pow_table(const uint64_t (*e)[4], const int* shift, uint32_t* const* out,
+                             int njobs, const uint32_t* Z, cudaStream_t stream) {
+    for (int b = 0; b < njobs; b += kMaxPowJobs) {
+        PowTabJobs jobs{};
+        const int cnt = njobs - b < kMaxPowJobs ? njobs - b : kMaxPowJobs;
+        for (int q = 0; q < cnt; ++q) {
+            for (int w = 0; w < 4; ++w) jobs.job[q].e[w] = e[b + q][w];
+            jobs.job[q].shift = shift[b + q];
+            jobs.job[q].out = out[b + q];
+        }
         count_launch();
-        mulmod_kernel<<<(half + kMulWarps - 1) / kMulWarps, 32 * kMulWarps, 0, stream>>>(
-            T, half, half, Q + b * kPolyN);
+        pow_table_kernel<<<cnt, 32 * kPowTabWarps, 0, stream>>>(jobs, Z);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t* Tt,
+                          cudaStream_t stream) {
+    const int warps = levels * kRows;
     count_launch();
-    t_transpose_kernel<<<kJPad, kRows, 0, stream>>>(T, Tt);
+    tables_kernel<<<(warps + kTabWarps - 1) / kTabWarps, 32 * kTabWarps, 0, stream>>>(Q, levels,
+                                                                                     Tab, Tt);
     return cudaGetLastError();
 }
 
@@ -386,15 +563,29 @@ cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, 
     return cudaGetLastError();
 }
 
+cudaError_t launch_level(const ranmar_state* in, uint64_t count, const uint32_t* Tab,
+                         uint32_t c_lvl, ranmar_state* out, uint32_t* outW, uint32_t* outV,
+                         cudaStream_t stream) {
+    const uint64_t blocks = (count + kApplyItems - 1) / kApplyItems;
+    count_launch();
+    if (outW)
+        level_kernel<true><<<static_cast<unsigned>(blocks), kApplyItems * 25, 0, stream>>>(
+            in, count, Tab, c_lvl, out, outW, outV);
+    else
+        level_kernel<false><<<static_cast<unsigned>(blocks), kApplyItems * 13, 0, stream>>>(
+            in, count, Tab, c_lvl, out, outW, outV);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_put_state(const ranmar_state& s, ranmar_state* dst, cudaStream_t stream) {
     count_launch();
     put_state_kernel<<<1, 128, 0, stream>>>(s, dst);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bulk(const ranmar_state* anchors, uint64_t H, const uint32_t* Tt,
-                        ranmar_state* out, uint64_t first, uint64_t n, uint32_t v_base,
-                        uint32_t jm, const ranmar_state& base, int sm_count, cudaStream_t stream) {
+cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
+                        uint64_t first, uint64_t n, uint32_t v_base, uint32_t jm,
+                        const ranmar_state& base, int sm_count, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -402,7 +593,7 @@ cudaError_t launch_bulk(const ranmar_state* anchors, uint64_t H, const uint32_t*
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    BulkArgs a{anchors, H, Tt, out, first, n, v_base, jm, base};
+    BulkArgs a{W1, H, Tt, out, first, n, v_base, jm, base};
     const uint64_t grid = H < uint64_t(2 * sm_count) ? H : uint64_t(2 * sm_count);
     count_launch();
     bulk_kernel<<<static_cast<unsigned>(grid), kBulkThreads, kBulkSmem, stream>>>(a);

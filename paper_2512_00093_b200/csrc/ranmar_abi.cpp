@@ -33,11 +33,15 @@ cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
-cudaError_t launch_t_table(uint32_t*, uint32_t*, const uint32_t*, cudaStream_t);
+cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
+                             const uint32_t*, cudaStream_t);
+cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
                          cudaStream_t);
+cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
+                         uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
-cudaError_t launch_bulk(const ranmar_state*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
+cudaError_t launch_bulk(const uint32_t*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
                         uint64_t, uint32_t, uint32_t, const ranmar_state&, int, cudaStream_t);
 std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
@@ -52,7 +56,10 @@ constexpr uint32_t kStart = 362436u;
 constexpr uint32_t kMaxSeed = 900000000u;
 constexpr int kRows = 128;      // must match jump_kernels.cu
 constexpr int kPolyN = 97;
-constexpr int kJPad = 104;
+constexpr int kWAnchor = 196;   // words per anchor extension row (jump_kernels.cu)
+constexpr int kSquares = 320;   // Z_k = t^(2^k), k < 320 (exponents < 2^256, shifts < 64)
+constexpr int kMaxLevels = 10;  // 128^9 = 2^63 streams
+constexpr int kMaxPlanPows = 7 * kMaxLevels + 1;
 
 static_assert(sizeof(ranmar_state) == 400, "ranmar_state must be the 400-B RanmarState");
 static_assert(sizeof(ranmar_gauss_state) == 416, "ranmar_gauss_state layout");
@@ -131,35 +138,76 @@ int device_status_ptr(uint32_t** out, int* sms) {
     return RANMAR_OK;
 }
 
+// ---- per-device square table Z_k = t^(2^k) mod phi (k < kSquares) --------
+// The squaring half of square-and-multiply, independent of any J: built once
+// per device by pow_kernel's squaring chain and kept for the process.
+uint32_t* g_squares[64] = {};
+
+int square_table(const uint32_t** out, cudaStream_t s) {
+    int dev = 0;
+    RB_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(RANMAR_ECUDA, "ranmar: device index out of range");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_squares[dev]) {
+        uint32_t* z = nullptr;
+        RB_CUDA(cudaMalloc(&z, size_t(kSquares) * kPolyN * 4), "cudaMalloc(squares)");
+        rb::PowJobs jobs{};
+        jobs.job[0].e[0] = 1;  // t^1, then kSquares - 1 squarings
+        jobs.job[0].extra = kSquares - 1;
+        jobs.job[0].out = z;
+        RB_CUDA(rb::launch_pow(jobs, 1, s), "pow_kernel launch (square table)");
+        RB_CUDA(cudaStreamSynchronize(s), "square table build");
+        g_squares[dev] = z;
+    }
+    *out = g_squares[dev];
+    return RANMAR_OK;
+}
+
 // ---- make_streams workspace plan -----------------------------------------
+// Stream starts form a base-128 tree: level L holds count[L] = ceil(n / 128^L)
+// states spaced 128^L J apart; the top level (128^top >= n) is the single
+// state s_{first J}. Level 1 is kept as 193-word extensions for the bulk.
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Plan {
-    uint64_t H;     // anchors (ceil(n / 128))
-    int anchor_levels;
-    int B;          // Q_b = P_{2^b J}, b < B
-    size_t off_q, off_pfirst, off_t, off_tt, off_anchor, off_base, total;
+    int top;         // 128^top >= n, top >= 2
+    int tab_levels;  // tables Tab_0 .. Tab_{top-1}
+    uint64_t count[kMaxLevels];
+    size_t off_q, off_pfirst, off_tab, off_tt, off_a0, off_base, off_w1, off_v1;
+    size_t off_lvl[kMaxLevels];
+    size_t total;
 };
 
 Plan plan_for(uint64_t n) {
     Plan p{};
-    p.H = (n + kRows - 1) / kRows;
-    p.anchor_levels = 0;
-    while ((uint64_t(1) << p.anchor_levels) < p.H) ++p.anchor_levels;
-    p.B = 7 + p.anchor_levels;  // T table uses Q_0..Q_6; anchor level b uses Q_{b+7}
+    p.top = 1;
+    for (unsigned __int128 span = kRows; span < n; span *= kRows) ++p.top;
+    if (p.top < 2) p.top = 2;
+    p.tab_levels = p.top;
+    unsigned __int128 span = 1;
+    for (int L = 0; L < p.top; ++L, span *= kRows)
+        p.count[L] = static_cast<uint64_t>((n + span - 1) / span);
     size_t o = 0;
     p.off_q = o;
-    o = align256(o + size_t(p.B) * kPolyN * 4);
+    o = align256(o + size_t(7 * p.tab_levels) * kPolyN * 4);
     p.off_pfirst = o;
     o = align256(o + kPolyN * 4);
-    p.off_t = o;
-    o = align256(o + size_t(kRows) * kPolyN * 4);
+    p.off_tab = o;
+    o = align256(o + size_t(p.tab_levels) * kRows * kPolyN * 4);
     p.off_tt = o;
-    o = align256(o + size_t(kJPad) * kRows * 4);
-    p.off_anchor = o;
-    o = align256(o + size_t(p.H) * sizeof(ranmar_state));
+    o = align256(o + size_t(kPolyN) * kRows * 4);
+    p.off_a0 = o;
+    o = align256(o + sizeof(ranmar_state));
     p.off_base = o;
     o = align256(o + sizeof(ranmar_state));
+    p.off_w1 = o;
+    o = align256(o + size_t(p.count[1]) * kWAnchor * 4);
+    p.off_v1 = o;
+    o = align256(o + size_t(p.count[1]) * 4);
+    for (int L = 2; L < p.top; ++L) {
+        p.off_lvl[L] = o;
+        o = align256(o + size_t(p.count[L]) * sizeof(ranmar_state));
+    }
     p.total = o;
     return p;
 }
@@ -379,11 +427,13 @@ size_t ranmar_make_streams_workspace(uint64_t n) { return plan_for(n ? n : 1).to
 
 int ranmar_pow_t_mod_dev(const ranmar_jump_count* j, uint32_t* d_coeff, void* stream) {
     if (!j || !d_coeff) return fail(RANMAR_EINVAL, "ranmar: null argument");
-    rb::PowJobs jobs{};
-    std::memcpy(jobs.job[0].e, j->limb, sizeof jobs.job[0].e);
-    jobs.job[0].extra = 0;
-    jobs.job[0].out = d_coeff;
-    RB_CUDA(rb::launch_pow(jobs, 1, static_cast<cudaStream_t>(stream)), "pow_kernel launch");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t* Z = nullptr;
+    if (int rc = square_table(&Z, s)) return rc;
+    const uint64_t(*e)[4] = &j->limb;
+    const int shift = 0;
+    uint32_t* out = d_coeff;
+    RB_CUDA(rb::launch_pow_table(e, &shift, &out, 1, Z, s), "pow_table_kernel launch");
     return RANMAR_OK;
 }
 
@@ -428,50 +478,65 @@ int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j
     if (int rc = device_status_ptr(&status, &sms)) return rc;
     (void)status;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t* Z = nullptr;
+    if (int rc = square_table(&Z, s)) return rc;
     char* ws = static_cast<char*>(d_ws);
     uint32_t* Q = reinterpret_cast<uint32_t*>(ws + p.off_q);
     uint32_t* Pf = reinterpret_cast<uint32_t*>(ws + p.off_pfirst);
-    uint32_t* T = reinterpret_cast<uint32_t*>(ws + p.off_t);
+    uint32_t* Tab = reinterpret_cast<uint32_t*>(ws + p.off_tab);
     uint32_t* Tt = reinterpret_cast<uint32_t*>(ws + p.off_tt);
-    ranmar_state* A = reinterpret_cast<ranmar_state*>(ws + p.off_anchor);
+    ranmar_state* A0 = reinterpret_cast<ranmar_state*>(ws + p.off_a0);
     ranmar_state* dbase = reinterpret_cast<ranmar_state*>(ws + p.off_base);
+    uint32_t* W1 = reinterpret_cast<uint32_t*>(ws + p.off_w1);
+    uint32_t* V1 = reinterpret_cast<uint32_t*>(ws + p.off_v1);
 
-    // K3a: Q_b = P_{2^b J} (b < B) and, if first > 0, P_{first J}.
-    rb::PowJobs jobs{};
-    std::memcpy(jobs.job[0].e, J.w, sizeof J.w);
-    jobs.job[0].extra = p.B - 1;
-    jobs.job[0].out = Q;
-    int njobs = 1;
-    if (first > 0) {
-        std::memcpy(jobs.job[1].e, fj.w, sizeof fj.w);
-        jobs.job[1].extra = 0;
-        jobs.job[1].out = Pf;
-        njobs = 2;
+    // K3a: Q_b = P_{2^b J} = prod_{k in bits(J)} Z_{k+b} for b < 7 * levels and,
+    // if first > 0, P_{first J}; all independent, one launch.
+    uint64_t e[kMaxPlanPows][4];
+    int shift[kMaxPlanPows];
+    uint32_t* outs[kMaxPlanPows];
+    int njobs = 0;
+    for (int b = 0; b < 7 * p.tab_levels; ++b, ++njobs) {
+        std::memcpy(e[njobs], J.w, sizeof J.w);
+        shift[njobs] = b;
+        outs[njobs] = Q + size_t(b) * kPolyN;
     }
-    RB_CUDA(rb::launch_pow(jobs, njobs, s), "pow_kernel launch");
-    // Offset table T_r = P_{rJ}, r < 128, by doubling.
-    RB_CUDA(rb::launch_t_table(T, Tt, Q, s), "t_table launch");
-    // Anchors A_h = s_{(first + 128 h) J}: A_0, then doubling with Q_{b+7}.
+    if (first > 0) {
+        std::memcpy(e[njobs], fj.w, sizeof fj.w);
+        shift[njobs] = 0;
+        outs[njobs] = Pf;
+        ++njobs;
+    }
+    RB_CUDA(rb::launch_pow_table(e, shift, outs, njobs, Z, s), "pow_table_kernel launch");
+    // Offset tables Tab_L[r] = P_{r 128^L J}.
+    RB_CUDA(rb::launch_tables(Q, p.tab_levels, Tab, Tt, s), "tables_kernel launch");
+    // A_0 = s_{first J}.
     const uint32_t jm = mod_u32(J, kMod);
     if (first == 0) {
-        RB_CUDA(rb::launch_put_state(*base, A, s), "put_state launch");
+        RB_CUDA(rb::launch_put_state(*base, A0, s), "put_state launch");
     } else {
         RB_CUDA(rb::launch_put_state(*base, dbase, s), "put_state launch");
         const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(first % kMod, jm, kMod)));
-        RB_CUDA(rb::launch_apply(dbase, A, 1, Pf, dec, s), "apply_kernel launch");
+        RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, s), "apply_kernel launch");
     }
-    for (int b = 0; b < p.anchor_levels; ++b) {
-        const uint64_t half = uint64_t(1) << b;
-        const uint64_t count = std::min<uint64_t>(half, p.H - half);
-        // jump by 2^b * 128 * J: (2^(b+7) mod m) * (J mod m) mod m
-        uint64_t pw = 1;
-        for (int x = 0; x < b + 7; ++x) pw = pw * 2 % kMod;
-        const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(pw, jm, kMod)));
-        RB_CUDA(rb::launch_apply(A, A + half, count, Q + size_t(b + 7) * kPolyN, dec, s),
-                "apply_kernel launch");
+    // Levels L-1 .. 1 of the base-128 tree (level 1 writes the anchors'
+    // extensions for the bulk kernel), then level 0.
+    const ranmar_state* in = A0;
+    for (int L = p.top - 1; L >= 1; --L) {
+        uint64_t pw = 1;  // 128^L mod m
+        for (int x = 0; x < L; ++x) pw = pw * 128 % kMod;
+        const uint32_t c_lvl = static_cast<uint32_t>(mulmod(pw, jm, kMod));
+        const uint64_t count = p.count[L];
+        const uint32_t* tab = Tab + size_t(L) * kRows * kPolyN;
+        if (L == 1) {
+            RB_CUDA(rb::launch_level(in, count, tab, c_lvl, nullptr, W1, V1, s), "level launch");
+        } else {
+            ranmar_state* o = reinterpret_cast<ranmar_state*>(ws + p.off_lvl[L]);
+            RB_CUDA(rb::launch_level(in, count, tab, c_lvl, o, nullptr, nullptr, s), "level launch");
+            in = o;
+        }
     }
-    // Bulk: every stream start.
-    RB_CUDA(rb::launch_bulk(A, p.H, Tt, d_out, first, n, base->v, jm, *base, sms, s),
+    RB_CUDA(rb::launch_bulk(W1, p.count[1], Tt, d_out, first, n, base->v, jm, *base, sms, s),
             "bulk_kernel launch");
     return RANMAR_OK;
 }
