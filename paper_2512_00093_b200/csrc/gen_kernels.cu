@@ -239,129 +239,6 @@ __global__ void __launch_bounds__(32 * kConsumeWarps)
     flush_hist(hw, gh, false, flushed);
 }
 
-// K4: thread per atom; the 97-word ring lives in shared memory column-major
-// (slot s of thread t at s * blockDim + t), so every access of a warp hits 32
-// distinct banks whatever the cursor. gaussian() is the repo's convention
-// (oracle/ranmar_oracle.c or_gaussian): polar method, v = 2u - 1, reject
-// rsq >= 1 or rsq == 0, return v2 * fac and cache v1 * fac.
-constexpr int kGaussThreads = 128;
-
-// gaussian()'s log: the repo convention's fixed IEEE sequence (see
-// oracle/ranmar_oracle.c or_glog for the derivation), written with explicit
-// round-to-nearest intrinsics so nvcc cannot contract or reorder anything and
-// the device result is bit-identical to the CPU definition.
-__device__ __forceinline__ double glog(double x) {
-    const long long b = __double_as_longlong(x);
-    int k = static_cast<int>((b >> 52) & 0x7FF) - 1023;
-    double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-    if (m > 0x1.6a09e667f3bcdp+0) {
-        m = __dmul_rn(m, 0.5);
-        k += 1;
-    }
-    const double f = __dsub_rn(m, 1.0);
-    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
-    const double z = __dmul_rn(s, s);
-    double p = 0x1.8618618618618p-5;
-    p = __fma_rn(p, z, 0x1.af286bca1af28p-5);
-    p = __fma_rn(p, z, 0x1.e1e1e1e1e1e1ep-5);
-    p = __fma_rn(p, z, 0x1.1111111111111p-4);
-    p = __fma_rn(p, z, 0x1.3b13b13b13b14p-4);
-    p = __fma_rn(p, z, 0x1.745d1745d1746p-4);
-    p = __fma_rn(p, z, 0x1.c71c71c71c71cp-4);
-    p = __fma_rn(p, z, 0x1.2492492492492p-3);
-    p = __fma_rn(p, z, 0x1.999999999999ap-3);
-    p = __fma_rn(p, z, 0x1.5555555555555p-2);
-    const double t = __dmul_rn(s, z);
-    const double l1p = __dmul_rn(2.0, __fma_rn(t, p, s));
-    const double kd = static_cast<double>(k);
-    return __fma_rn(kd, 0x1.62e42fefa3800p-1, __fma_rn(kd, 0x1.ef35793c76730p-45, l1p));
-}
-
-struct RingGen {
-    uint32_t* ring;  // column base for this thread
-    int i;           // cursor (j = i - 64 mod 97)
-    uint32_t v;
-
-    __device__ __forceinline__ uint32_t next() {
-        const int j = i >= 64 ? i - 64 : i + 33;
-        const uint32_t u = ring[i * kGaussThreads] - ring[j * kGaussThreads];
-        ring[i * kGaussThreads] = u;
-        i = i == 0 ? 96 : i - 1;
-        v = add_mod_m(v, kStepA);
-        return (u - v) & kMask;
-    }
-};
-
-__global__ void __launch_bounds__(kGaussThreads)
-    gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
-                    uint64_t steps, double* __restrict__ out, uint32_t* status) {
-    extern __shared__ uint32_t ring_smem[];  // 97 x kGaussThreads
-    constexpr int kWords = sizeof(ranmar_gauss_state) / 4;  // 104
-    const uint64_t a0 = static_cast<uint64_t>(blockIdx.x) * kGaussThreads;
-    const int count = static_cast<int>((n_atoms - a0 < (uint64_t)kGaussThreads ? n_atoms - a0 : (uint64_t)kGaussThreads));
-    const uint64_t a = a0 + threadIdx.x;
-    const bool active = static_cast<int>(threadIdx.x) < count;
-
-    // Coalesced transpose of the block's lanes into the column-major rings.
-    const uint32_t* gw = reinterpret_cast<const uint32_t*>(g + a0);
-    for (int w = threadIdx.x; w < count * kWords; w += kGaussThreads) {
-        const int atom = w / kWords, field = w - atom * kWords;
-        if (field < 97) ring_smem[field * kGaussThreads + atom] = gw[w];
-    }
-    __syncthreads();
-
-    int i0 = 0, j0 = 0;
-    uint32_t v0 = 0;
-    bool ok = false;
-    double saved = 0.0;
-    bool has = false;
-    if (active) {
-        i0 = g[a].s.i;
-        j0 = g[a].s.j;
-        v0 = g[a].s.v;
-        saved = g[a].saved;
-        has = g[a].has_saved != 0;
-        ok = state_ok(i0, j0, v0);
-        if (!ok) atomicOr(status, kStatusBadState);
-    }
-    RingGen gen{ring_smem + threadIdx.x, i0, v0};
-    if (ok) {
-        for (uint64_t st = 0; st < steps; ++st) {
-            double* o = out + (st * n_atoms + a) * per_step;
-            for (uint64_t c = 0; c < per_step; ++c) {
-                double g_out;
-                if (has) {
-                    has = false;
-                    g_out = saved;
-                } else {
-                    double v1, v2, rsq;
-                    do {  // v = 2u - 1 and rsq are exact in binary64 (<= 48 bits)
-                        v1 = __dsub_rn(__dmul_rn(static_cast<double>(gen.next()), 0x1p-23), 1.0);
-                        v2 = __dsub_rn(__dmul_rn(static_cast<double>(gen.next()), 0x1p-23), 1.0);
-                        rsq = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
-                    } while (rsq >= 1.0 || rsq == 0.0);
-                    const double fac = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glog(rsq)), rsq));
-                    saved = __dmul_rn(v1, fac);
-                    has = true;
-                    g_out = __dmul_rn(v2, fac);
-                }
-                st_cs(o + c, g_out);
-            }
-        }
-        g[a].s.i = gen.i;
-        g[a].s.j = gen.i >= 64 ? gen.i - 64 : gen.i + 33;
-        g[a].s.v = gen.v;
-        g[a].saved = saved;
-        g[a].has_saved = has ? 1u : 0u;
-    }
-    __syncthreads();
-    uint32_t* gww = reinterpret_cast<uint32_t*>(g + a0);
-    for (int w = threadIdx.x; w < count * kWords; w += kGaussThreads) {
-        const int atom = w / kWords, field = w - atom * kWords;
-        if (field < 97) gww[w] = ring_smem[field * kGaussThreads + atom] & kMask;
-    }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -399,25 +276,6 @@ cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t 
     count_launch();
     consume_kernel<<<static_cast<unsigned>(blocks), 32 * kConsumeWarps, smem, stream>>>(
         d_states, n_streams, per_stream, d_sums, d_hist, status);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
-                            uint64_t steps, double* d_out, uint32_t* status,
-                            cudaStream_t stream) {
-    if (n_atoms == 0) return cudaSuccess;
-    const int smem = 97 * kGaussThreads * 4;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gaussian_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    const uint64_t blocks = (n_atoms + kGaussThreads - 1) / kGaussThreads;
-    count_launch();
-    gaussian_kernel<<<static_cast<unsigned>(blocks), kGaussThreads, smem, stream>>>(
-        d_g, n_atoms, per_step, steps, d_out, status);
     return cudaGetLastError();
 }
 

@@ -34,6 +34,7 @@ void count_launch(int n = 1);
 
 // Status bits OR-ed into the library's device status word.
 constexpr uint32_t kStatusBadState = 1u;          // cursor separation / range violated
+constexpr uint32_t kStatusInternal = 2u;          // an internal invariant failed (bug)
 
 static_assert(sizeof(ranmar_state) == 400, "ranmar_state must match ranmar::RanmarState");
 

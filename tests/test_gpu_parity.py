@@ -286,6 +286,28 @@ def test_gaussian_odd_count_keeps_cache(oracle):
         assert ulp_diff(out.reshape(-1), exp.reshape(-1)).max() <= 1
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
     assert (gh["has_saved"] == og["has_saved"]).all()
+    assert gh.tobytes() == og.tobytes()  # states, cursors, cached deviate
+
+
+@pytest.mark.parametrize("per_step,steps", [(1, 1), (2, 3), (3, 100), (7, 40), (300, 2), (257, 1),
+                                            (5, 77)])
+def test_gaussian_shapes(oracle, per_step, steps):
+    # chunking of the staged output, odd/even deviate counts, the unstaged path
+    # (per_step > 256), atoms not a multiple of the block, random cursor phase
+    # and a pre-filled cache on some atoms.
+    from oracle.bind import GAUSS_DTYPE
+    n = 37
+    base = random_states(n, per_step * 1000 + steps, oracle)
+    og = np.zeros(n, GAUSS_DTYPE)
+    og["s"] = base
+    og["has_saved"][::3] = 1
+    og["saved"][::3] = np.linspace(-2, 2, len(og[::3]))
+    g = torch.from_numpy(og.copy().view(np.int32).reshape(n, rb.GAUSS_WORDS)).cuda()
+    out = rb.gaussian(g, per_step, steps).cpu().numpy()
+    exp = oracle.gaussian_fill(og, per_step, steps)
+    assert ulp_diff(out.reshape(-1), exp.reshape(-1)).max() == 0
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    assert gh.tobytes() == og.tobytes()
 
 
 # ------------------------------------------------------ invariants, host API

@@ -50,11 +50,11 @@ def main():
         for _ in range(reps):
             rb.consume(st, 1 << 20)
     else:
-        n = 1 << 22
+        n = 1 << 20
         st = rb.make_streams(7, 2**50, n)
         g = rb.gauss_states_from(st)
         for _ in range(reps):
-            rb.gaussian(g, 3, 10)
+            rb.gaussian(g, 3, 100)
     torch.cuda.synchronize()
     assert rb.device_status() == 0
     print(f"{args.case} ok, launches={rb.kernel_launches()}")
