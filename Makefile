@@ -12,7 +12,7 @@ OBJS := $(BUILD)/gen_kernels.o $(BUILD)/gauss_kernel.o $(BUILD)/jump_kernels.o $
 HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh
 
 .PHONY: all lib oracle ref clean sass
-all: lib oracle
+all: lib oracle facade
 
 lib: $(LIB)
 
@@ -39,3 +39,9 @@ sass: $(LIB)
 
 clean:
 	rm -rf $(BUILD) $(PKG)/lib
+
+# C++ drop-in facade check (run on a GPU by tests/test_gpu_facade.py)
+FACADE := tests/cpp/facade_test
+facade: $(FACADE)
+$(FACADE): tests/cpp/facade_test.cpp include/ranmar_b200.hpp $(LIB)
+	g++ -O2 -std=c++20 -Iinclude $< -L$(PKG)/lib -lranmar_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -o $@

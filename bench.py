@@ -134,14 +134,8 @@ def max_over_ranks(x: float, world: int) -> float:
 
 def gather_checksums(sums, world: int):
     """NCCL all-gather of per-rank checksums (after the timed region only)."""
-    import torch
-    if world == 1:
-        return [sums]
-    import torch.distributed as dist
-    t = torch.tensor(sums, dtype=torch.int64, device="cuda")
-    out = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
-    return [o.tolist() for o in out]
+    from paper_2512_00093_b200.shard import gather_u64
+    return gather_u64(sums, device="cuda")
 
 
 def load_traffic(kernel_key: str):
@@ -218,7 +212,8 @@ def run_ours(args, rank, world, local):
 
     # ---- config 2: make_streams + 2^32 fp32 stored, per rank ----
     n, per = C2["n"], C2["per"]
-    first = rank * n
+    from paper_2512_00093_b200.shard import weak_range
+    first, _ = weak_range(n, rank)
     base = rb.init(C2["seed"])
     states = torch.empty((n, rb.STATE_WORDS), dtype=torch.int32, device=dev)
     ws = torch.empty(rb.lib().ranmar_make_streams_workspace(n), dtype=torch.uint8, device=dev)
@@ -266,7 +261,8 @@ def run_ours(args, rank, world, local):
     # checksum of this rank's last step, gathered over NCCL after timing
     with torch.cuda.stream(stream):
         chk = int((out.view(n, per)[:, :1024].double() * 2**24).sum().item())
-    sums = gather_checksums([chk, first], world)
+    torch.cuda.synchronize()
+    sums = gather_checksums([first, chk], world)
 
     # ---- e2e: the same job through the host-buffer C-ABI path ----
     e2e = None

@@ -1,0 +1,43 @@
+"""Stream-range partitioner for one process per GPU.
+
+The streams of make_streams(base, J, N) are independent units (jump.hpp:97-104:
+StreamMode::independent is "safe to compute concurrently"), so rank r of W
+simply owns a contiguous range and derives its own starts s_{kJ} from the seed
+with ranmar_make_streams_dev(first=range.start). There is no exchange on the
+data path; collectives only gather per-rank checksums after the timed region.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+
+def stream_range(n_total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Balanced contiguous split: (first, count) of rank `rank` (strong scaling)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def weak_range(n_per_rank: int, rank: int) -> Tuple[int, int]:
+    """Weak scaling: every rank owns n_per_rank streams of one global sequence."""
+    return rank * n_per_rank, n_per_rank
+
+
+def gather_u64(values: Sequence[int], device=None) -> List[List[int]]:
+    """All-gather a short list of u64 checksums from every rank (torch.distributed;
+    NCCL on GPUs, gloo on CPU). Values are carried as int64 bit patterns."""
+    import torch
+    import torch.distributed as dist
+
+    def to_i64(x: int) -> int:
+        x &= (1 << 64) - 1
+        return x - (1 << 64) if x >= 1 << 63 else x
+
+    t = torch.tensor([to_i64(v) for v in values], dtype=torch.int64, device=device)
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [[v & ((1 << 64) - 1) for v in t.tolist()]]
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [[v & ((1 << 64) - 1) for v in o.tolist()] for o in out]
