@@ -1,7 +1,7 @@
-// Generation kernels (sm_100a): K1 store (u32 / f32 / f64), K2 consume
-// (per-stream sum + histogram, nothing stored), K4 gaussian (polar).
+// Generation kernel K1 (sm_100a): stored uniforms (u32 / f32 / f64).
+// (K2 consume: consume_kernel.cu; K4 gaussian: gauss_kernel.cu.)
 //
-// K1/K2 mapping — one warp per stream, 32 consecutive outputs per round.
+// Mapping — one warp per stream, 32 consecutive outputs per round.
 // Both lags are 1 mod 32 (97 = 3*32 + 1, 33 = 32 + 1), so with
 //   y[r][l] = x_{32 r + l}
 // the recurrence x_n = x_{n-97} - x_{n-33} (core.hpp:56; Alg. 2)
@@ -145,100 +145,6 @@ __global__ void __launch_bounds__(32 * kGenWarps)
     });
 }
 
-// K2: per-lane private u16 counters, lane l owning bank l:
-//   word((b >> 1) * 32 + l), half (b & 1)
-// so a warp's 32 updates never conflict and need no atomics. A lane sees at
-// most kFlushRounds outputs between flushes, so u16 cannot overflow.
-constexpr int kConsumeWarps = 4;
-constexpr uint32_t kHistWordsPerWarp = 128 * 32;  // 256 u16 bins x 32 lanes = 16 KB
-constexpr uint64_t kFlushRounds = 65535;
-
-__device__ __forceinline__ void flush_hist(uint32_t* hw, uint32_t* __restrict__ ghist, bool zero,
-                                           bool accumulate) {
-    __syncwarp();
-    const int l = threadIdx.x & 31;
-    // Lane l reduces bins l, l+32, ..., l+224 over the 32 lane columns.
-#pragma unroll 1
-    for (int b = l; b < 256; b += 32) {
-        const unsigned short* col =
-            reinterpret_cast<const unsigned short*>(hw + (b >> 1) * 32) + (b & 1);
-        uint32_t s = 0;
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) s += col[2 * c];
-        ghist[b] = accumulate ? ghist[b] + s : s;
-    }
-    __syncwarp();
-    if (zero)
-        for (uint32_t w = l; w < kHistWordsPerWarp; w += 32) hw[w] = 0;
-    __syncwarp();
-}
-
-// Histogram update for one output u (24-bit): byte offset of bin u >> 16 in
-// this lane's column, ((bin >> 1) * 32 words) * 4 + (bin & 1) * 2.
-__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u) {
-    // hb: 32-bit shared-window address of this lane's column
-    const uint32_t a = hb + (((u >> 10) & 0x3F80u) | ((u >> 15) & 2u));
-    uint32_t c;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(a));
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(c + 1) : "memory");
-}
-
-__global__ void __launch_bounds__(32 * kConsumeWarps)
-    consume_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
-                   uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status) {
-    extern __shared__ uint32_t smem_hist[];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kConsumeWarps + w;
-    if (k >= n_streams) return;
-    uint32_t* hw = smem_hist + w * kHistWordsPerWarp;
-    for (uint32_t i = l; i < kHistWordsPerWarp; i += 32) hw[i] = 0;
-    __syncwarp();
-    const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hw)) + 4 * l;
-    uint32_t* gh = hist + k * 256;
-
-    WarpGen g;
-    if (!g.load(states + k, status)) return;
-    const uint64_t N = per_stream, full = N >> 5;
-    const uint32_t tail = static_cast<uint32_t>(N & 31);
-    uint64_t sum64 = 0;
-    bool flushed = false;
-    uint64_t r = 0;
-    while (r < full) {
-        // <= kFlushRounds rounds between flushes (u16 counters), sums in
-        // blocks of <= 128 rounds (128 x 24-bit values fit 32 bits).
-        const uint64_t chunk_end = min(full, r + kFlushRounds);
-        while (r < chunk_end) {
-            const uint64_t left = chunk_end - r;
-            const uint32_t blk = left < 128 ? static_cast<uint32_t>(left) : 128u;
-            uint32_t s32 = 0;
-#pragma unroll 4
-            for (uint32_t q = 0; q < blk; ++q) {
-                const uint32_t u = g.round() & kMask;
-                s32 += u;
-                hist_add(hb, u);
-            }
-            sum64 += s32;
-            r += blk;
-        }
-        if (r < full || tail) {
-            flush_hist(hw, gh, true, flushed);
-            flushed = true;
-        }
-    }
-    if (tail) {
-        const uint32_t u = g.round() & kMask;
-        if (static_cast<uint32_t>(l) < tail) {
-            sum64 += u;
-            hist_add(hb, u);
-        }
-    }
-    g.store(states + k, N, full + (tail ? 1 : 0));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum64 += __shfl_xor_sync(0xffffffffu, sum64, o);
-    if (l == 0) sums[k] = sum64;
-    flush_hist(hw, gh, false, flushed);
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -259,24 +165,5 @@ template cudaError_t launch_generate<float>(ranmar_state*, uint64_t, uint64_t, f
                                             cudaStream_t);
 template cudaError_t launch_generate<double>(ranmar_state*, uint64_t, uint64_t, double*,
                                              uint32_t*, cudaStream_t);
-
-cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
-                           uint64_t* d_sums, uint32_t* d_hist, uint32_t* status,
-                           cudaStream_t stream) {
-    if (n_streams == 0) return cudaSuccess;
-    const int smem = kConsumeWarps * kHistWordsPerWarp * 4;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(consume_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    const uint64_t blocks = (n_streams + kConsumeWarps - 1) / kConsumeWarps;
-    count_launch();
-    consume_kernel<<<static_cast<unsigned>(blocks), 32 * kConsumeWarps, smem, stream>>>(
-        d_states, n_streams, per_stream, d_sums, d_hist, status);
-    return cudaGetLastError();
-}
 
 }  // namespace rb

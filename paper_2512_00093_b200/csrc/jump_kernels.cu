@@ -133,15 +133,29 @@ __global__ void __launch_bounds__(kPowThreads) pow_kernel(PowJobs jobs) {
 }
 
 // ---- warp-level product mod phi: out = a * b (a, b, out in shared memory,
-// out may alias a; c is a 193-word scratch). 9,409 MACs, then the fold.
+// out may alias a; c is a 320-word scratch). 9,409 MACs, then the fold.
+// i-outer: lane l accumulates c[l + 32q] (q < 7) for every a_i at once, reading
+// b from a zero-padded copy (bz[96 + j] = b_j) so no lane needs a range test;
+// 7 independent accumulators per lane instead of one long dependent chain.
+constexpr int kMulScratch = 320;
+
 __device__ __forceinline__ void warp_mulmod(const uint32_t* a, const uint32_t* b, uint32_t* c,
                                             uint32_t* out, int l) {
-    for (int k = l; k < 193; k += 32) {
-        const int lo = k > 96 ? k - 96 : 0, hi = k < 96 ? k : 96;
-        uint32_t acc = 0;
-        for (int i = lo; i <= hi; ++i) acc += a[i] * b[k - i];
-        c[k] = acc;
+    uint32_t* bz = c;  // [0, 320): zeros, b at 96..192, zeros
+    for (int k = l; k < kMulScratch; k += 32) bz[k] = (k >= 96 && k < 193) ? b[k - 96] : 0u;
+    __syncwarp();
+    uint32_t acc[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+    for (int i = 0; i < kPolyN; ++i) {
+        const uint32_t ai = a[i];
+        const uint32_t* bi = bz + 96 + l - i;  // bz[96 + (l + 32q) - i] = b_{k - i}
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc[q] += ai * bi[32 * q];
     }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+        if (l + 32 * q < 193) c[l + 32 * q] = acc[q];
     __syncwarp();
     fold_to(c, out, l, 32, [] { __syncwarp(); });
 }
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
     pow_table_kernel(const __grid_constant__ PowTabJobs jobs, const uint32_t* __restrict__ Z) {
     __shared__ uint32_t acc[kPowTabWarps][kPolyN];
     __shared__ uint32_t fac[kPowTabWarps][kPolyN];
-    __shared__ uint32_t scr[kPowTabWarps][193];
+    __shared__ uint32_t scr[kPowTabWarps][kMulScratch];
     __shared__ int used[kPowTabWarps];
     const PowTabJob& job = jobs.job[blockIdx.x];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(32 * kTabWarps)
                   uint32_t* __restrict__ Tt) {
     __shared__ uint32_t acc[kTabWarps][kPolyN];
     __shared__ uint32_t fac[kTabWarps][kPolyN];
-    __shared__ uint32_t scr[kTabWarps][193];
+    __shared__ uint32_t scr[kTabWarps][kMulScratch];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int gw = blockIdx.x * kTabWarps + w;
     if (gw >= levels * kRows) return;
