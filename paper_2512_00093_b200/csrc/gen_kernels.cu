@@ -106,8 +106,13 @@ __device__ __forceinline__ void warp_stream(ranmar_state* st, uint64_t N, uint32
     if (!g.load(st, status)) return;
     const uint64_t full = N >> 5;
     const uint32_t tail = static_cast<uint32_t>(N & 31);
-#pragma unroll 4
-    for (uint64_t r = 0; r < full; ++r) emit(r, g.round(), true);
+    // 32-bit inner counter, unrolled by 8: the only per-round work left is
+    // the generator, the conversion and the store
+    for (uint64_t r0 = 0; r0 < full; r0 += (1u << 30)) {
+        const uint32_t cnt = static_cast<uint32_t>(full - r0 < (1u << 30) ? full - r0 : (1u << 30));
+#pragma unroll 8
+        for (uint32_t r = 0; r < cnt; ++r) emit(r0 + r, g.round(), true);
+    }
     if (tail) emit(full, g.round(), static_cast<uint32_t>(g.l) < tail);
     g.store(st, N, full + (tail ? 1 : 0));
 }

@@ -9,11 +9,11 @@
 // modular integer arithmetic, not a float contraction.
 //
 //  pow_kernel        K3a  the squaring chain t^(2^k) mod phi in shared memory
-//                         (one CTA): symmetric squaring (4,753 MACs instead of
-//                         9,409) and the trinomial fold split into three
-//                         conflict-free phases (sources [160,192], [127,159],
-//                         [97,126]). Run once per device to fill the square
-//                         table Z_k = t^(2^k), k < 320.
+//                         (one CTA, 256 threads split the 9,409 MACs of each
+//                         product four ways) and the trinomial fold split into
+//                         three conflict-free phases (sources [160,192],
+//                         [127,159], [97,126]). Run once per device to fill
+//                         the square table Z_k = t^(2^k), k < 320.
 //  pow_table_kernel  K3a  the multiply half: t^(E 2^s) = prod_{k in bits(E)}
 //                         Z_{k+s} (right-to-left square-and-multiply with the
 //                         cached squares), one CTA per exponent, warps reduce
@@ -78,18 +78,46 @@ __device__ __forceinline__ void fold_to(uint32_t* c, uint32_t* a, int t, int nt,
     sync();
 }
 
-__device__ __forceinline__ void block_square(uint32_t* a, uint32_t* c) {
+// CTA-level product out = a * b mod phi for exactly 256 threads: four groups
+// of 64 threads each take a quarter of a's coefficients, thread tt of a group
+// accumulates c[tt], c[tt + 64], c[tt + 128] over its quarter reading b from a
+// zero-padded copy (no range tests), the quarters are summed, then folded.
+// Shared scratch: bz[320] + part[4][193] + c[193]. out may alias a or b.
+struct BlockMulScratch {
+    uint32_t bz[320];
+    uint32_t part[4][193];
+    uint32_t c[193];
+};
+
+__device__ __forceinline__ void block_mulmod(const uint32_t* a, const uint32_t* b, uint32_t* out,
+                                             BlockMulScratch& s) {
     const int t = threadIdx.x;
-    for (int k = t; k < 193; k += blockDim.x) {
-        const int lo = k > 96 ? k - 96 : 0;
-        uint32_t acc = 0;
-        for (int i = lo; 2 * i < k; ++i) acc += a[i] * a[k - i];
-        acc <<= 1;
-        if ((k & 1) == 0) acc += a[k >> 1] * a[k >> 1];
-        c[k] = acc;
-    }
+    for (int k = t; k < 320; k += 256) s.bz[k] = (k >= 96 && k < 193) ? b[k - 96] : 0u;
     __syncthreads();
-    fold_to(c, a, t, blockDim.x, [] { __syncthreads(); });
+    const int g = t >> 6, tt = t & 63;
+    const int i0 = 25 * g, i1 = i0 + 25 < kPolyN ? i0 + 25 : kPolyN;
+    uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+#pragma unroll 5
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t ai = a[i];
+        const uint32_t* bi = s.bz + 96 + tt - i;
+        acc0 += ai * bi[0];
+        acc1 += ai * bi[64];
+        acc2 += ai * bi[128];
+        acc3 += ai * bi[192];  // only used by tt == 0 (c[192])
+    }
+    s.part[g][tt] = acc0;
+    s.part[g][tt + 64] = acc1;
+    s.part[g][tt + 128] = acc2;
+    if (tt == 0) s.part[g][192] = acc3;
+    __syncthreads();
+    if (t < 193) s.c[t] = s.part[0][t] + s.part[1][t] + s.part[2][t] + s.part[3][t];
+    __syncthreads();
+    fold_to(s.c, out, t, 256, [] { __syncthreads(); });
+}
+
+__device__ __forceinline__ void block_square(uint32_t* a, BlockMulScratch& s) {
+    block_mulmod(a, a, a, s);
 }
 
 // a <- a * t (polyring.hpp:101-109)
@@ -107,7 +135,7 @@ __device__ __forceinline__ bool ebit(const uint64_t* e, int b) { return (e[b >> 
 
 __global__ void __launch_bounds__(kPowThreads) pow_kernel(PowJobs jobs) {
     __shared__ uint32_t a[kPolyN];
-    __shared__ uint32_t c[193];
+    __shared__ BlockMulScratch c;
     const PowJob& job = jobs.job[blockIdx.x];
     int msb = -1;
     for (int w = 3; w >= 0 && msb < 0; --w)
@@ -223,28 +251,31 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
 
 // ---- offset tables: Tab_L[r] = P_{r 128^L J} = prod_{b in bits(r)} Q_{7L + b}
 // (warp per entry); Tab_0 also written transposed for the bulk kernel.
-constexpr int kTabWarps = 4;
-
-__global__ void __launch_bounds__(32 * kTabWarps)
-    tables_kernel(const uint32_t* __restrict__ Q, int levels, uint32_t* __restrict__ Tab,
+// One CTA per entry: its <= 6 products run at CTA speed (the chain is the
+// latency of the whole setup, not the few MACs).
+__global__ void __launch_bounds__(256)
+    tables_kernel(const uint32_t* __restrict__ Q, uint32_t* __restrict__ Tab,
                   uint32_t* __restrict__ Tt) {
-    __shared__ uint32_t acc[kTabWarps][kPolyN];
-    __shared__ uint32_t fac[kTabWarps][kPolyN];
-    __shared__ uint32_t scr[kTabWarps][kMulScratch];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int gw = blockIdx.x * kTabWarps + w;
-    if (gw >= levels * kRows) return;
-    const int lvl = gw / kRows, r = gw % kRows;
-    for (int k = l; k < kPolyN; k += 32) acc[w][k] = (k == 0);
-    __syncwarp();
-    for (int b = 0; b < 7; ++b) {
+    __shared__ uint32_t acc[kPolyN];
+    __shared__ uint32_t fac[kPolyN];
+    __shared__ BlockMulScratch scr;
+    const int e = blockIdx.x, t = threadIdx.x;
+    const int lvl = e / kRows, r = e % kRows;
+    int first = -1;  // lowest set bit of r: start from that factor directly
+    for (int b = 0; b < 7 && first < 0; ++b)
+        if ((r >> b) & 1) first = b;
+    for (int k = t; k < kPolyN; k += 256)
+        acc[k] = first < 0 ? (k == 0) : Q[static_cast<size_t>(7 * lvl + first) * kPolyN + k];
+    __syncthreads();
+    for (int b = first + 1; first >= 0 && b < 7; ++b) {
         if (!((r >> b) & 1)) continue;
-        warp_load_poly(fac[w], Q + static_cast<size_t>(7 * lvl + b) * kPolyN, l);
-        warp_mulmod(acc[w], fac[w], scr[w], acc[w], l);
+        for (int k = t; k < kPolyN; k += 256) fac[k] = Q[static_cast<size_t>(7 * lvl + b) * kPolyN + k];
+        __syncthreads();
+        block_mulmod(acc, fac, acc, scr);
     }
-    for (int k = l; k < kPolyN; k += 32) {
-        Tab[static_cast<size_t>(gw) * kPolyN + k] = acc[w][k];
-        if (lvl == 0) Tt[k * kRows + r] = acc[w][k];
+    for (int k = t; k < kPolyN; k += 256) {
+        Tab[static_cast<size_t>(e) * kPolyN + k] = acc[k];
+        if (lvl == 0) Tt[k * kRows + r] = acc[k];
     }
 }
 
@@ -561,10 +592,8 @@ cudaError_t launch_pow_table(const uint64_t (*e)[4], const int* shift, uint32_t*
 
 cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t* Tt,
                           cudaStream_t stream) {
-    const int warps = levels * kRows;
     count_launch();
-    tables_kernel<<<(warps + kTabWarps - 1) / kTabWarps, 32 * kTabWarps, 0, stream>>>(Q, levels,
-                                                                                     Tab, Tt);
+    tables_kernel<<<levels * kRows, 256, 0, stream>>>(Q, Tab, Tt);
     return cudaGetLastError();
 }
 
