@@ -339,3 +339,23 @@ def test_host_buffer_context(oracle):
     with pytest.raises(ValueError):
         ctx.make_streams(900000001, 5, 2)
     ctx.close()
+
+
+def test_make_streams_dense_jump_counts_and_determinism(oracle):
+    # Jump counts with ~half their bits set exercise every product path of the
+    # square-table exponentiation and the offset tables; repeated runs must be
+    # byte-identical (a cheap race detector: compute-sanitizer is unavailable).
+    rng = random.Random(17)
+    base = oracle.init(2024)
+    for bits in (37, 64, 131):
+        j = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+        ref = None
+        for _ in range(4):
+            got = rb.states_to_host(rb.make_streams_dev(base, j, 300, first=11))
+            if ref is None:
+                ref = got
+                exp = oracle.make_streams(base, j, 300, first=11)
+                assert got.tobytes() == exp.tobytes(), bits
+            assert got.tobytes() == ref.tobytes()
+        assert rb.pow_t_mod_dev(j).cpu().numpy().view(np.uint32).tolist() == \
+            oracle.pow_t_mod(j).tolist()
