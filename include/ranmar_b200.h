@@ -134,6 +134,12 @@ int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_
 int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, void* stream);
 
+/* The same gaussian() calls for FEW streams with MANY calls each: one warp per
+ * stream (serves the scalar RanMars-style facade). d_out[s * count + q] is
+ * call q of stream s. States and cached deviates advance in place. */
+int ranmar_gaussian_stream_f64_dev(ranmar_gauss_state* d_g, uint64_t n_streams, uint64_t count,
+                                   double* d_out, void* stream);
+
 /* Sticky status bits of the current device (bit 0: a kernel met a state with
  * bad cursors / v >= m). Synchronises the device. clear != 0 resets them. */
 int ranmar_device_status(uint32_t* flags, int clear);
@@ -159,6 +165,10 @@ int ranmar_ctx_generate_f32(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n_
                             uint64_t per_stream, float* h_out);
 int ranmar_ctx_consume(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n_streams,
                        uint64_t per_stream, uint64_t* h_sums, uint32_t* h_hist);
+/* count gaussian() calls on each of n HOST gauss states (advanced in place),
+ * h_out[s * count + q]; one warp per stream on the device. */
+int ranmar_ctx_gaussian_stream(ranmar_ctx* ctx, ranmar_gauss_state* h_g, uint64_t n_streams,
+                               uint64_t count, double* h_out);
 /* Bytes moved host->device and device->host by the last ctx call. */
 int ranmar_ctx_last_traffic(ranmar_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 

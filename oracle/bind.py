@@ -82,6 +82,7 @@ class Oracle:
             "or_consume": (None, [vp, u64, u64, vp, vp]),
             "or_gaussian_fill": (None, [vp, u64, u64, u64, vp]),
             "or_glog": (C.c_double, [C.c_double]),
+            "or_gaussian": (C.c_double, [vp]),
             "or_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
             "or_from_text": (i32, [C.c_char_p, vp]),
         }
@@ -196,6 +197,16 @@ class Oracle:
 
     def glog(self, x: float) -> float:
         return self.lib.or_glog(x)
+
+    def gaussian_call(self, g: np.ndarray) -> float:
+        """One gaussian() call on a 1-element GAUSS_DTYPE array (advanced in place)."""
+        return self.lib.or_gaussian(_p(g))
+
+    def uniform_call(self, g: np.ndarray) -> float:
+        """One uniform() = next_f64 call on the stream of a GAUSS_DTYPE record."""
+        out = np.empty(1, np.uint32)
+        self.lib.or_step_n(_p(g), 1, _p(out))  # s is at offset 0 of the record
+        return float(out[0]) * 2.0**-24
 
     def to_text(self, state: np.ndarray) -> str:
         buf = C.create_string_buffer(4096)

@@ -92,6 +92,8 @@ def lib() -> C.CDLL:
         "ranmar_ctx_generate_u32": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_generate_f32": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_consume": (i32, [vp, vp, u64, u64, vp, vp]),
+        "ranmar_gaussian_stream_f64_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_ctx_gaussian_stream": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_last_traffic": (i32, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
@@ -313,6 +315,18 @@ def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
     return out
 
 
+def gaussian_stream(gstates, count: int, out=None, stream=None):
+    """count gaussian() calls on each of a FEW streams (one warp per stream) ->
+    out[stream, q] (float64); states and cached deviates advance in place."""
+    torch = _torch()
+    n = gstates.shape[0]
+    if out is None:
+        out = torch.empty((n, count), dtype=torch.float64, device="cuda")
+    _check(lib().ranmar_gaussian_stream_f64_dev(_dptr(gstates), n, count, _dptr(out),
+                                                _stream_ptr(stream)))
+    return out
+
+
 def gauss_states_from(states_t):
     """[n,100] state tensor -> [n,104] ranmar_gauss_state tensor with an empty cache."""
     torch = _torch()
@@ -390,3 +404,95 @@ class Context:
         _check(lib().ranmar_ctx_consume(self._h, _ptr(states), len(states), per_stream,
                                         _ptr(sums), _ptr(hist)))
         return sums, hist
+
+    def gaussian_stream(self, gstates: np.ndarray, count: int) -> np.ndarray:
+        """count gaussian() calls on each host GAUSS_DTYPE state (advanced in place)."""
+        assert gstates.dtype == GAUSS_DTYPE and gstates.flags.c_contiguous
+        out = np.empty((len(gstates), count), np.float64)
+        _check(lib().ranmar_ctx_gaussian_stream(self._h, _ptr(gstates), len(gstates), count,
+                                                _ptr(out)))
+        return out
+
+
+class RanMars:
+    """LAMMPS-style generator object (the north star's "seed
+    constructor, uniform()/gaussian(), jump-ahead by J"): one stream whose
+    uniform() (= next_f64, core.hpp:70-72) and gaussian() (the repo convention)
+    calls return exactly the sequential values, served from blocks the GPU
+    generates (K1 for uniforms, the warp-per-stream K4s for deviates).
+
+    Blocks grow from 256 to `block` while one kind of call repeats; switching
+    kind (or asking for state()) re-derives the exact state after the values
+    already returned, so uniform()/gaussian() may be interleaved freely.
+    """
+
+    _MIN_BLOCK = 256
+
+    def __init__(self, seed: Optional[int] = None, state: Optional[np.ndarray] = None,
+                 block: int = 1 << 16, device: int = 0, ctx: Optional["Context"] = None):
+        if (seed is None) == (state is None):
+            raise ValueError("give exactly one of seed or state")
+        self._ctx = ctx or Context(device)
+        self._g = np.zeros(1, GAUSS_DTYPE)
+        self._g["s"] = init(seed) if seed is not None else np.asarray(state, STATE_DTYPE).reshape(1)
+        self._max_block = max(self._MIN_BLOCK, int(block))
+        self._kind = None   # 'u' or 'g': what _buf holds
+        self._buf = None
+        self._pos = 0
+        self._next = None   # state after the whole buffer
+        self._size = self._MIN_BLOCK
+
+    # -- buffers ----------------------------------------------------------
+    def _run(self, kind: str, g: np.ndarray, n: int) -> np.ndarray:
+        """n values of `kind` from gauss state g (advanced in place)."""
+        if kind == "u":
+            s = np.ascontiguousarray(g["s"])
+            u = self._ctx.generate(s, n, "u32")
+            g["s"] = s
+            return u.astype(np.float64) * 2.0**-24
+        return self._ctx.gaussian_stream(g, n)[0]
+
+    def _sync(self):
+        """Make _g the exact state after the values returned so far."""
+        if self._kind is not None:
+            if self._pos == len(self._buf):
+                self._g = self._next
+            elif self._pos > 0:
+                g = self._g.copy()
+                self._run(self._kind, g, self._pos)
+                self._g = g
+        self._kind, self._buf, self._pos, self._next = None, None, 0, None
+
+    def _take(self, kind: str) -> float:
+        if self._kind != kind or self._pos == len(self._buf):
+            if self._kind == kind:  # same kind, buffer used up: grow
+                self._size = min(2 * self._size, self._max_block)
+            else:
+                self._size = self._MIN_BLOCK
+            self._sync()
+            nxt = self._g.copy()
+            self._buf = self._run(kind, nxt, self._size)
+            self._next, self._kind, self._pos = nxt, kind, 0
+        x = float(self._buf[self._pos])
+        self._pos += 1
+        return x
+
+    # -- the interface ----------------------------------------------------
+    def uniform(self) -> float:
+        """Next uniform in [0, 1): next_f64 (core.hpp:70-72)."""
+        return self._take("u")
+
+    def gaussian(self) -> float:
+        """Next standard normal deviate (repo convention)."""
+        return self._take("g")
+
+    def jump(self, j) -> None:
+        """Advance the stream by J uniforms (jump_state, jump.hpp:90-95); a cached
+        gaussian deviate, if any, is kept."""
+        self._sync()
+        self._g["s"] = self._ctx.jump(np.ascontiguousarray(self._g["s"]), j)
+
+    def state(self) -> np.ndarray:
+        """1-element GAUSS_DTYPE record: the stream state and cached deviate."""
+        self._sync()
+        return self._g.copy()

@@ -30,6 +30,8 @@ template <class T>
 cudaError_t launch_generate(ranmar_state*, uint64_t, uint64_t, T*, uint32_t*, cudaStream_t);
 cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_t*, uint32_t*,
                            cudaStream_t);
+cudaError_t launch_gaussian_stream(ranmar_gauss_state*, uint64_t, uint64_t, double*, uint32_t*,
+                                   cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
@@ -600,6 +602,17 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     return RANMAR_OK;
 }
 
+int ranmar_gaussian_stream_f64_dev(ranmar_gauss_state* d_g, uint64_t n_streams, uint64_t count,
+                                   double* d_out, void* stream) {
+    if (n_streams && (!d_g || (count && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_gaussian_stream(d_g, n_streams, count, d_out, status,
+                                       static_cast<cudaStream_t>(stream)),
+            "gaussian_stream_kernel launch");
+    return RANMAR_OK;
+}
+
 int ranmar_device_status(uint32_t* flags, int clear) {
     RB_STATUS_PTR(status);
     RB_CUDA(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
@@ -618,7 +631,7 @@ struct ranmar_ctx {
     cudaStream_t st[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     void* dbuf[2] = {nullptr, nullptr};  // per-slot output chunk
-    size_t dbuf_bytes = 0;
+    size_t dbuf_bytes[2] = {0, 0};
     ranmar_state* dstates = nullptr;
     size_t dstates_n = 0;
     void* dws = nullptr;
@@ -665,12 +678,8 @@ int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per
     uint64_t chunk = stream_bytes ? std::max<uint64_t>(1, kChunkBytes / stream_bytes) : n;
     chunk = std::min<uint64_t>(chunk, n);
     if (int rc = ctx_states(c, n)) return rc;
-    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes, chunk * stream_bytes)) return rc;
-    if (c->dbuf[1] == nullptr || c->dbuf_bytes < chunk * stream_bytes) {
-        if (c->dbuf[1]) cudaFree(c->dbuf[1]);
-        c->dbuf[1] = nullptr;
-        RB_CUDA(cudaMalloc(&c->dbuf[1], c->dbuf_bytes), "cudaMalloc(ctx)");
-    }
+    for (int b = 0; b < 2; ++b)  // one output buffer per pipeline slot
+        if (int rc = ctx_reserve(&c->dbuf[b], &c->dbuf_bytes[b], chunk * stream_bytes)) return rc;
     RB_CUDA(cudaMemcpyAsync(c->dstates, h_states, n * sizeof(ranmar_state),
                             cudaMemcpyHostToDevice, c->st[0]),
             "H2D states");
@@ -814,7 +823,7 @@ int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64
     RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
     if (int rc = ctx_states(c, n)) return rc;
     const size_t need = n * (8 + 256 * 4);
-    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes, need)) return rc;
+    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], need)) return rc;
     uint64_t* dsums = static_cast<uint64_t*>(c->dbuf[0]);
     uint32_t* dhist = reinterpret_cast<uint32_t*>(dsums + n);
     cudaStream_t s = c->st[0];
@@ -829,6 +838,32 @@ int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64
                             s),
             "D2H states");
     c->d2h += n * (8 + 256 * 4 + sizeof(ranmar_state));
+    RB_CUDA(cudaStreamSynchronize(s), "sync");
+    return RANMAR_OK;
+}
+
+int ranmar_ctx_gaussian_stream(ranmar_ctx* c, ranmar_gauss_state* h_g, uint64_t n, uint64_t count,
+                               double* h_out) {
+    if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
+    c->h2d = c->d2h = 0;
+    if (n == 0) return RANMAR_OK;
+    if (!h_g || (count && !h_out)) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    for (uint64_t k = 0; k < n; ++k)
+        if (!host_state_ok(h_g[k].s))
+            return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
+                                           " violates cursor/residue invariants");
+    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t gbytes = n * sizeof(ranmar_gauss_state), obytes = n * count * sizeof(double);
+    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], gbytes + obytes)) return rc;
+    ranmar_gauss_state* dg = static_cast<ranmar_gauss_state*>(c->dbuf[0]);
+    double* dout = reinterpret_cast<double*>(static_cast<char*>(c->dbuf[0]) + gbytes);
+    cudaStream_t s = c->st[0];
+    RB_CUDA(cudaMemcpyAsync(dg, h_g, gbytes, cudaMemcpyHostToDevice, s), "H2D gauss states");
+    c->h2d += gbytes;
+    if (int rc = ranmar_gaussian_stream_f64_dev(dg, n, count, dout, s)) return rc;
+    if (obytes) RB_CUDA(cudaMemcpyAsync(h_out, dout, obytes, cudaMemcpyDeviceToHost, s), "D2H out");
+    RB_CUDA(cudaMemcpyAsync(h_g, dg, gbytes, cudaMemcpyDeviceToHost, s), "D2H gauss states");
+    c->d2h += gbytes + obytes;
     RB_CUDA(cudaStreamSynchronize(s), "sync");
     return RANMAR_OK;
 }

@@ -1,7 +1,8 @@
 """GPU parity: the sm_100a kernels, called through the C ABI, against the oracle
 (oracle/ranmar_oracle.c, itself pinned to the reference) and the reference's
-golden vectors. Integer/byte results must be bit-exact; gaussian() is within
-1 ulp (the only non-exact step is log(): CUDA's vs glibc's)."""
+golden vectors. Integer/byte results must be bit-exact; gaussian() must be
+within the north star's 1 ulp of the repo convention (it is 0 ulp: the
+convention's log() is a fixed IEEE sequence reproduced on the device)."""
 import random
 
 import numpy as np
