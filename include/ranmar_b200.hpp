@@ -16,6 +16,8 @@
 //   step(state) / next_f64(state), one at a time   UniformStream (device-
 //                                                  filled buffer) and bulk
 //                                                  generate_f32 / generate_u32
+//   (north star: LAMMPS RanMars seed constructor,  RanMars: uniform(), gaussian(),
+//    uniform()/gaussian(), jump-ahead)             jump(J), state()
 //
 // std::invalid_argument is thrown exactly where the reference throws it;
 // CUDA failures throw std::runtime_error. Scalar step() has no GPU analogue
@@ -289,6 +291,90 @@ class UniformStream {
     std::vector<std::uint32_t> buf_;
     std::size_t pos_ = 0;
     mutable std::vector<std::uint32_t> scratch_;
+};
+
+// LAMMPS-style generator object: seed constructor,
+// uniform() (= next_f64), gaussian() (the repo's polar convention, DESIGN.md
+// §5) and jump-ahead, all on one stream. Values come from blocks the GPU
+// generates (K1 for uniforms, the warp-per-stream gaussian kernel for
+// deviates); blocks grow from 256 to `block` while one kind of call repeats,
+// and switching kind re-derives the exact state, so calls interleave freely.
+class RanMars {
+ public:
+    explicit RanMars(std::uint32_t seed, std::size_t block = 1 << 16)
+        : RanMars(init(seed), block) {}
+    explicit RanMars(const RanmarState& s, std::size_t block = 1 << 16)
+        : max_block_(block < kMinBlock ? kMinBlock : block) {
+        std::memset(&g_, 0, sizeof g_);
+        g_.s = *detail::abi(&s);
+    }
+
+    double uniform() { return take(Kind::uniform); }
+    double gaussian() { return take(Kind::gaussian); }
+
+    // jump_state (jump.hpp:90-95) on the stream; a cached deviate is kept.
+    void jump(const JumpCount& j) {
+        sync();
+        detail::check(ranmar_ctx_jump(detail::context(), &g_.s, &g_.s, 1, &j.abi()));
+    }
+
+    // Stream state after the values returned so far.
+    RanmarState state() {
+        sync();
+        RanmarState s;
+        *detail::abi(&s) = g_.s;
+        return s;
+    }
+    bool has_saved() {
+        sync();
+        return g_.has_saved != 0;
+    }
+
+ private:
+    enum class Kind { none, uniform, gaussian };
+    static constexpr std::size_t kMinBlock = 256;
+
+    void run(Kind k, ranmar_gauss_state& g, std::size_t n, std::vector<double>& out) {
+        out.resize(n);
+        if (k == Kind::uniform) {
+            std::vector<std::uint32_t> u(n);
+            detail::check(ranmar_ctx_generate_u32(detail::context(), &g.s, 1, n, u.data()));
+            for (std::size_t q = 0; q < n; ++q) out[q] = static_cast<double>(u[q]) * 0x1p-24;
+        } else {
+            detail::check(ranmar_ctx_gaussian_stream(detail::context(), &g, 1, n, out.data()));
+        }
+    }
+    void sync() {
+        if (kind_ != Kind::none) {
+            if (pos_ == buf_.size()) {
+                g_ = next_;
+            } else if (pos_ > 0) {
+                std::vector<double> scratch;
+                run(kind_, g_, pos_, scratch);
+            }
+        }
+        kind_ = Kind::none;
+        buf_.clear();
+        pos_ = 0;
+    }
+    double take(Kind k) {
+        if (kind_ != k || pos_ == buf_.size()) {
+            size_ = (kind_ == k) ? (2 * size_ < max_block_ ? 2 * size_ : max_block_) : kMinBlock;
+            sync();
+            next_ = g_;
+            run(k, next_, size_, buf_);
+            kind_ = k;
+        }
+        return buf_[pos_++];
+    }
+
+    ranmar_gauss_state g_{};     // state at the start of buf_
+    ranmar_gauss_state next_{};  // state after all of buf_
+    Kind kind_ = Kind::none;
+    std::vector<double> buf_;
+    std::size_t pos_ = 0;
+    std::size_t size_ = kMinBlock;
+    std::size_t max_block_;
 };
 
 }  // namespace ranmar

@@ -82,6 +82,24 @@ int main() {
         auto f = generate_f32(st2, 8);
         CHECK(f.size() == 24 && f[0] >= 0.0f && f[0] < 1.0f);
     }
+    // RanMars-style object: uniform() is next_f64 of the stream; gaussian()
+    // interleaves on the same stream (values pinned by the Python tests)
+    {
+        RanMars r(12345u, 1024);
+        CHECK(r.uniform() == 1905444 * 0x1p-24);
+        CHECK(r.uniform() == 14595391 * 0x1p-24);
+        const double g1 = r.gaussian();
+        CHECK(g1 > -10.0 && g1 < 10.0);
+        CHECK(r.has_saved());          // the second deviate of the pair is cached
+        const double g2 = r.gaussian();
+        CHECK(!r.has_saved() && g2 > -10.0 && g2 < 10.0);
+        RanMars same(12345u, 4096);    // another block size, same sequence
+        same.uniform();
+        same.uniform();
+        CHECK(same.gaussian() == g1 && same.gaussian() == g2);
+        CHECK(same.state() == r.state());
+        CHECK(throws_invalid([] { RanMars bad(900000001u); }));
+    }
     // serialize.hpp round trip
     {
         const auto s = jump_state(init(4711), JumpCount(1) << 100);
