@@ -140,6 +140,21 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
 int ranmar_gaussian_stream_f64_dev(ranmar_gauss_state* d_g, uint64_t n_streams, uint64_t count,
                                    double* d_out, void* stream);
 
+/* Device-side persistence (bulk serialize.hpp:21-136). to_text: d_text gets
+ * the concatenated "ranmar24 v1" texts of n device states, d_offsets[0..n]
+ * their start offsets (d_offsets[n] = total bytes); text_cap must be at least
+ * ranmar_to_text_bound(n). from_text: parses texts [d_offsets[k],
+ * d_offsets[k+1]) with the reference's strict rules; d_err[k] = 0 or the
+ * 1-based line of the first error (where from_text throws invalid_argument),
+ * d_states[k] written only on success. */
+uint64_t ranmar_to_text_bound(uint64_t n);
+size_t ranmar_text_workspace(uint64_t n);
+int ranmar_to_text_dev(const ranmar_state* d_states, uint64_t n, char* d_text, uint64_t text_cap,
+                       uint64_t* d_offsets, void* d_workspace, size_t workspace_bytes,
+                       void* stream);
+int ranmar_from_text_dev(const char* d_text, const uint64_t* d_offsets, uint64_t n,
+                         ranmar_state* d_states, int32_t* d_err, void* stream);
+
 /* Sticky status bits of the current device (bit 0: a kernel met a state with
  * bad cursors / v >= m). Synchronises the device. clear != 0 resets them. */
 int ranmar_device_status(uint32_t* flags, int clear);

@@ -93,6 +93,10 @@ def lib() -> C.CDLL:
         "ranmar_ctx_generate_f32": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_consume": (i32, [vp, vp, u64, u64, vp, vp]),
         "ranmar_gaussian_stream_f64_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_to_text_bound": (u64, [u64]),
+        "ranmar_text_workspace": (sz, [u64]),
+        "ranmar_to_text_dev": (i32, [vp, u64, vp, u64, vp, vp, sz, vp]),
+        "ranmar_from_text_dev": (i32, [vp, vp, u64, vp, vp, vp]),
         "ranmar_ctx_gaussian_stream": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_last_traffic": (i32, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
@@ -325,6 +329,39 @@ def gaussian_stream(gstates, count: int, out=None, stream=None):
     _check(lib().ranmar_gaussian_stream_f64_dev(_dptr(gstates), n, count, _dptr(out),
                                                 _stream_ptr(stream)))
     return out
+
+
+def to_text_dev(states, stream=None):
+    """Bulk ranmar::to_text (serialize.hpp:21-40) on the GPU.
+    Returns (text: uint8 CUDA tensor, offsets: int64 CUDA tensor [n + 1])."""
+    torch = _torch()
+    n = states.shape[0]
+    text = torch.empty(int(lib().ranmar_to_text_bound(n)), dtype=torch.uint8, device="cuda")
+    off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(lib().ranmar_text_workspace(n)), dtype=torch.uint8, device="cuda")
+    _check(lib().ranmar_to_text_dev(_dptr(states), n, _dptr(text), text.numel(), _dptr(off),
+                                    _dptr(ws), ws.numel(), _stream_ptr(stream)))
+    return text, off
+
+
+def from_text_dev(text, offsets, stream=None):
+    """Bulk ranmar::from_text (serialize.hpp:81-136) on the GPU: texts
+    [offsets[k], offsets[k+1]) of `text` -> (states [n, 100], err [n]); err[k]
+    is 0 or the 1-based line where the reference's parser throws."""
+    torch = _torch()
+    n = offsets.shape[0] - 1
+    states = torch.zeros((n, STATE_WORDS), dtype=torch.int32, device="cuda")
+    err = torch.empty(n, dtype=torch.int32, device="cuda")
+    _check(lib().ranmar_from_text_dev(_dptr(text), _dptr(offsets), n, _dptr(states), _dptr(err),
+                                      _stream_ptr(stream)))
+    return states, err
+
+
+def texts_to_host(text, offsets) -> list:
+    """(text, offsets) from to_text_dev -> list of Python strings."""
+    off = offsets.cpu().numpy()
+    blob = text[: int(off[-1])].cpu().numpy().tobytes()
+    return [blob[off[k]:off[k + 1]].decode() for k in range(len(off) - 1)]
 
 
 def gauss_states_from(states_t):

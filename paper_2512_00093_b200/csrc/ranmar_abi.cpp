@@ -32,6 +32,11 @@ cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_
                            cudaStream_t);
 cudaError_t launch_gaussian_stream(ranmar_gauss_state*, uint64_t, uint64_t, double*, uint32_t*,
                                    cudaStream_t);
+uint64_t text_bound(uint64_t);
+size_t text_workspace(uint64_t);
+cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void*, cudaStream_t);
+cudaError_t launch_from_text(const char*, const uint64_t*, uint64_t, ranmar_state*, int32_t*,
+                             cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
@@ -599,6 +604,29 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
             "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+uint64_t ranmar_to_text_bound(uint64_t n) { return rb::text_bound(n); }
+size_t ranmar_text_workspace(uint64_t n) { return rb::text_workspace(n); }
+
+int ranmar_to_text_dev(const ranmar_state* d_states, uint64_t n, char* d_text, uint64_t text_cap,
+                       uint64_t* d_offsets, void* d_ws, size_t ws_bytes, void* stream) {
+    if (n == 0) return RANMAR_OK;
+    if (!d_states || !d_text || !d_offsets || !d_ws) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (text_cap < rb::text_bound(n)) return fail(RANMAR_ENOMEM, "ranmar: text buffer below ranmar_to_text_bound(n)");
+    if (ws_bytes < rb::text_workspace(n)) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
+    RB_CUDA(rb::launch_to_text(d_states, n, d_text, d_offsets, d_ws, static_cast<cudaStream_t>(stream)),
+            "to_text kernels launch");
+    return RANMAR_OK;
+}
+
+int ranmar_from_text_dev(const char* d_text, const uint64_t* d_offsets, uint64_t n,
+                         ranmar_state* d_states, int32_t* d_err, void* stream) {
+    if (n == 0) return RANMAR_OK;
+    if (!d_text || !d_offsets || !d_states || !d_err) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_CUDA(rb::launch_from_text(d_text, d_offsets, n, d_states, d_err, static_cast<cudaStream_t>(stream)),
+            "from_text_kernel launch");
     return RANMAR_OK;
 }
 

@@ -1,0 +1,301 @@
+// Device-side state persistence: bulk ranmar::to_text /
+// from_text (serialize.hpp:21-40 / :81-136) for arrays of device states, so
+// stream starts made on the GPU (e.g. config 3's 2^20) can be exported and
+// re-imported in the reference's "ranmar24 v1" text without a CPU loop.
+//
+//   text_len_kernel    thread per state: exact byte length of its text
+//   scan kernels       exclusive prefix sum of the lengths -> offsets
+//   to_text_kernel     warp per state: lane-parallel line formatting, the
+//                      line offsets by a warp prefix sum
+//   from_text_kernel   thread per state: the reference's strict parser
+//                      (same checks, same 1-based line numbers in the error)
+#include <cstdint>
+
+#include "ranmar_device.cuh"
+
+namespace rb {
+
+namespace {
+
+__device__ __forceinline__ int ndigits(uint32_t x) {
+    int d = 1;
+    while (x >= 10) {
+        x /= 10;
+        ++d;
+    }
+    return d;
+}
+
+__device__ __forceinline__ char* put_uint(char* p, uint32_t x) {
+    const int d = ndigits(x);
+    for (int k = d - 1; k >= 0; --k) {
+        p[k] = static_cast<char>('0' + x % 10);
+        x /= 10;
+    }
+    return p + d;
+}
+
+// serialize.hpp:21-40 line by line: 0 "ranmar24 v1", 1 "i <i+1> j <j+1>",
+// 2 "v <v>", 3 + k "u <k+1> <lane[k]>".
+__device__ __forceinline__ int line_len(const ranmar_state& s, int line) {
+    if (line == 0) return 12;
+    if (line == 1) return 2 + ndigits(s.i + 1) + 3 + ndigits(s.j + 1) + 1;
+    if (line == 2) return 2 + ndigits(s.v) + 1;
+    const int k = line - 3;
+    return 2 + ndigits(k + 1) + 1 + ndigits(s.lane[k]) + 1;
+}
+
+__device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* p) {
+    if (line == 0) {
+        const char m[] = "ranmar24 v1\n";
+        for (int c = 0; c < 12; ++c) p[c] = m[c];
+        return;
+    }
+    if (line == 1) {
+        *p++ = 'i';
+        *p++ = ' ';
+        p = put_uint(p, static_cast<uint32_t>(s.i + 1));
+        *p++ = ' ';
+        *p++ = 'j';
+        *p++ = ' ';
+        p = put_uint(p, static_cast<uint32_t>(s.j + 1));
+        *p = '\n';
+        return;
+    }
+    if (line == 2) {
+        *p++ = 'v';
+        *p++ = ' ';
+        p = put_uint(p, s.v);
+        *p = '\n';
+        return;
+    }
+    const int k = line - 3;
+    *p++ = 'u';
+    *p++ = ' ';
+    p = put_uint(p, static_cast<uint32_t>(k + 1));
+    *p++ = ' ';
+    p = put_uint(p, s.lane[k]);
+    *p = '\n';
+}
+
+__global__ void text_len_kernel(const ranmar_state* __restrict__ st, uint64_t n,
+                                uint64_t* __restrict__ len) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const ranmar_state& s = st[k];
+    uint64_t L = 0;
+    for (int line = 0; line < 100; ++line) L += line_len(s, line);
+    len[k] = L;
+}
+
+// exclusive scan, 1024 items per block; block totals to bsum
+constexpr int kScanT = 1024;
+__global__ void __launch_bounds__(kScanT)
+    scan_block_kernel(const uint64_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ out,
+                      uint64_t* __restrict__ bsum) {
+    __shared__ uint64_t warp_tot[32];
+    const int t = threadIdx.x, l = t & 31, w = t >> 5;
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kScanT + t;
+    const uint64_t x = k < n ? in[k] : 0;
+    uint64_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t v = warp_tot[l], wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (l >= o) wi += y;
+        }
+        warp_tot[l] = wi - v;  // exclusive warp offsets
+        if (l == 31 && bsum) bsum[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    if (k < n) out[k] = warp_tot[w] + incl - x;
+}
+
+// out[k] += boff[block] (if any) + *base (if any); then out[n] = out[n-1] + len[n-1]
+__global__ void scan_add_kernel(uint64_t* __restrict__ out, uint64_t n,
+                                const uint64_t* __restrict__ boff, const uint64_t* base) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kScanT + threadIdx.x;
+    if (k < n) out[k] += (boff ? boff[blockIdx.x] : 0) + (base ? *base : 0);
+}
+
+__global__ void total_kernel(uint64_t* __restrict__ off, uint64_t n, const uint64_t* __restrict__ len) {
+    off[n] = off[n - 1] + len[n - 1];
+}
+
+__global__ void copy_u64_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src) {
+    *dst = *src;
+}
+
+// warp per state: lane handles lines lane, lane+32, lane+64, lane+96
+__global__ void to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n,
+                               const uint64_t* __restrict__ off, char* __restrict__ text) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int l = threadIdx.x & 31;
+    if (k >= n) return;
+    const ranmar_state& s = st[k];
+    char* base = text + off[k];
+    uint32_t before = 0;  // bytes of the lines of previous passes
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+        const int line = pass * 32 + l;
+        const uint32_t len = line < 100 ? static_cast<uint32_t>(line_len(s, line)) : 0u;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (l >= o) incl += y;
+        }
+        if (line < 100) put_line(s, line, base + before + incl - len);
+        before += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// ---- parser (serialize.hpp:81-136), thread per state
+struct Cursor {
+    const char* p;
+    const char* end;
+};
+
+// next line without terminator; false at end of input
+__device__ __forceinline__ bool next_line(Cursor& c, const char*& b, const char*& e) {
+    if (c.p >= c.end) return false;
+    b = c.p;
+    const char* q = c.p;
+    while (q < c.end && *q != '\n') ++q;
+    e = q;
+    c.p = q < c.end ? q + 1 : q;
+    if (e > b && e[-1] == '\r') --e;
+    return true;
+}
+
+__device__ __forceinline__ bool take_uint(const char*& p, const char* e, uint64_t& v) {
+    v = 0;
+    int nd = 0;
+    while (p < e && *p >= '0' && *p <= '9') {
+        v = v * 10 + static_cast<uint64_t>(*p - '0');
+        if (v > 0xFFFFFFFFull) return false;
+        ++p;
+        ++nd;
+    }
+    return nd > 0;
+}
+
+__device__ __forceinline__ bool take_lit(const char*& p, const char* e, const char* lit, int n) {
+    if (e - p < n) return false;
+    for (int c = 0; c < n; ++c)
+        if (p[c] != lit[c]) return false;
+    p += n;
+    return true;
+}
+
+__global__ void from_text_kernel(const char* __restrict__ text, const uint64_t* __restrict__ off,
+                                 uint64_t n, ranmar_state* __restrict__ out,
+                                 int32_t* __restrict__ err) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    Cursor c{text + off[k], text + off[k + 1]};
+    ranmar_state s;
+    int line = 1;
+    const char *b, *e;
+    auto fail = [&](int ln) { err[k] = ln; };
+    if (!next_line(c, b, e) || !(e - b == 11 && take_lit(b, e, "ranmar24 v1", 11))) return fail(line);
+    ++line;
+    uint64_t i = 0, j = 0, v = 0;
+    if (!next_line(c, b, e) || !take_lit(b, e, "i ", 2) || !take_uint(b, e, i) ||
+        !take_lit(b, e, " j ", 3) || !take_uint(b, e, j) || b != e)
+        return fail(line);
+    if (i < 1 || i > 97 || j < 1 || j > 97 || (i + 97 - j) % 97 != 64) return fail(line);
+    ++line;
+    if (!next_line(c, b, e) || !take_lit(b, e, "v ", 2) || !take_uint(b, e, v) || b != e ||
+        v >= kMod)
+        return fail(line);
+    s.i = static_cast<int32_t>(i) - 1;
+    s.j = static_cast<int32_t>(j) - 1;
+    s.v = static_cast<uint32_t>(v);
+    for (int q = 0; q < 97; ++q) {
+        ++line;
+        uint64_t idx = 0, lane = 0;
+        if (!next_line(c, b, e) || !take_lit(b, e, "u ", 2) || !take_uint(b, e, idx) ||
+            !take_lit(b, e, " ", 1) || !take_uint(b, e, lane) || b != e ||
+            idx != static_cast<uint64_t>(q) + 1 || lane > kMask)
+            return fail(line);
+        s.lane[q] = static_cast<uint32_t>(lane);
+    }
+    for (const char* p = c.p; p < c.end; ++p)
+        if (*p != '\n' && *p != '\r' && *p != ' ' && *p != '\t') return fail(line + 1);
+    out[k] = s;
+    err[k] = 0;
+}
+
+}  // namespace
+
+// Upper bound of one state's text: 12 + 10 + 11 + 97 * 14.
+constexpr uint64_t kMaxStateText = 12 + 10 + 11 + 97 * 14;
+
+uint64_t text_bound(uint64_t n) { return n * kMaxStateText; }
+
+constexpr uint64_t kTextChunk = uint64_t(kScanT) * kScanT;  // states per scan (2^20)
+
+size_t text_workspace(uint64_t n) {
+    const uint64_t c = n < kTextChunk ? n : kTextChunk;
+    const uint64_t blocks = (c + kScanT - 1) / kScanT;
+    return static_cast<size_t>((c + 2 * blocks + 2) * sizeof(uint64_t));
+}
+
+// Offsets d_off[0..n] (d_off[n] = total bytes) and the concatenated texts;
+// chunks of 2^20 states, each continuing where the previous one ended.
+cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_text,
+                           uint64_t* d_off, void* d_ws, cudaStream_t stream) {
+    for (uint64_t c0 = 0; c0 < n; c0 += kTextChunk) {
+        const uint64_t m = n - c0 < kTextChunk ? n - c0 : kTextChunk;
+        const uint64_t blocks = (m + kScanT - 1) / kScanT;
+        uint64_t* len = static_cast<uint64_t*>(d_ws);
+        uint64_t* bsum = len + m;
+        uint64_t* boff = bsum + blocks;
+        uint64_t* off = d_off + c0;
+        const uint64_t* base = c0 ? d_off + c0 : nullptr;  // the previous chunk's total
+        // the previous chunk wrote off[c0] = its end; keep it as this chunk's base
+        uint64_t* base_copy = boff + blocks;
+        count_launch(3);
+        text_len_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, stream>>>(d_states + c0,
+                                                                                    m, len);
+        if (base) {
+            count_launch();
+            copy_u64_kernel<<<1, 1, 0, stream>>>(base_copy, base);
+        }
+        scan_block_kernel<<<static_cast<unsigned>(blocks), kScanT, 0, stream>>>(len, m, off, bsum);
+        if (blocks > 1) {
+            count_launch(2);
+            scan_block_kernel<<<1, kScanT, 0, stream>>>(bsum, blocks, boff, nullptr);
+            scan_add_kernel<<<static_cast<unsigned>(blocks), kScanT, 0, stream>>>(
+                off, m, boff, base ? base_copy : nullptr);
+        } else if (base) {
+            count_launch();
+            scan_add_kernel<<<1, kScanT, 0, stream>>>(off, m, nullptr, base_copy);
+        }
+        count_launch();
+        total_kernel<<<1, 1, 0, stream>>>(off, m, len);
+        to_text_kernel<<<static_cast<unsigned>((m + 7) / 8), 256, 0, stream>>>(d_states + c0, m,
+                                                                               off, d_text);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_from_text(const char* d_text, const uint64_t* d_off, uint64_t n,
+                             ranmar_state* d_states, int32_t* d_err, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    from_text_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(d_text, d_off, n,
+                                                                                 d_states, d_err);
+    return cudaGetLastError();
+}
+
+}  // namespace rb
