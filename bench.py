@@ -181,6 +181,27 @@ def cpu_reference_c2(steps: int = 1, threads: int | None = None):
             "seconds": t}
 
 
+def cpu_reference_text(states: np.ndarray):
+    """The reference's to_text / from_text on all host cores, on a sample."""
+    from oracle.bind import Reference, reference_available
+    if not reference_available():
+        return None
+    ref, threads = Reference(), os.cpu_count() or 1
+    t0 = time.perf_counter()
+    buf, total = ref.to_text_bulk(states, threads)
+    t1 = time.perf_counter()
+    texts = [bytes(buf[k * 1408:(k + 1) * 1408]).rstrip(b"\0") for k in range(len(states))]
+    blob = np.frombuffer(b"".join(texts), np.uint8)
+    offs = np.cumsum([0] + [len(t) for t in texts]).astype(np.uint64)
+    t2 = time.perf_counter()
+    _, bad = ref.from_text_bulk(blob, offs, threads)
+    t3 = time.perf_counter()
+    assert bad == 0
+    return {"to_text_states_per_s": len(states) / (t1 - t0),
+            "from_text_states_per_s": len(states) / (t3 - t2), "cores": threads,
+            "sample": f"{len(states)} states"}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -328,8 +349,33 @@ def run_ours(args, rank, world, local):
             "workload": "make_streams(init_unchecked(987654321), 2^120): 2^20 stream starts s_{kJ} per rank",
             "jump_aheads_per_s": n3 * world / (ms3 * 1e-3), "ms": ms3,
             "batched_jump_state_per_s": n3 * world / (msj * 1e-3), "batched_jump_ms": msj,
-            "macs_per_start": 2 * 97 * 97}
-        del st3, ws3, jo
+            "macs_per_start_bulk": 97 * 97}
+        # §8f row 1: export / re-import the 2^20 starts as reference text on the device
+        text, off = rb.to_text_dev(st3, stream=stream)
+        back, err = rb.from_text_dev(text, off, stream=stream)
+        torch.cuda.synchronize()
+        assert int(err.abs().sum()) == 0 and torch.equal(back, st3)
+        tb = int(off[-1].item())
+        a.record(stream)
+        for _ in range(reps):
+            rb.to_text_dev(st3, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_tt = max_over_ranks(a.elapsed_time(b) / reps, world)
+        a.record(stream)
+        for _ in range(reps):
+            rb.from_text_dev(text, off, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_ft = max_over_ranks(a.elapsed_time(b) / reps, world)
+        extras["persistence"] = {
+            "workload": "to_text / from_text of config 3's 2^20 stream starts (reference text format)",
+            "text_bytes": tb, "to_text_states_per_s": n3 * world / (ms_tt * 1e-3),
+            "from_text_states_per_s": n3 * world / (ms_ft * 1e-3),
+            "to_text_ms": ms_tt, "from_text_ms": ms_ft}
+        if world == 1 and not args.no_cpu:
+            extras["persistence"]["cpu_reference"] = cpu_reference_text(rb.states_to_host(st3[:1 << 16]))
+        del st3, ws3, jo, text, off, back, err
 
     # ---- config 4: consume in kernel (no store) ----
     if not args.quick:

@@ -247,6 +247,8 @@ class Reference:
             "ref_jump_batch": (i32, [vp, u64, vp, i32, vp]),
             "ref_consume": (i32, [vp, vp, u64, u64, u64, i32, vp, vp]),
             "ref_last_error": (C.c_char_p, []),
+            "ref_to_text_bulk": (C.c_long, [vp, u64, vp, C.c_long, i32]),
+            "ref_from_text_bulk": (C.c_long, [vp, vp, u64, vp, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -330,6 +332,23 @@ class Reference:
         limbs = np.zeros(4, np.uint64)
         self._check(self.lib.ref_parse_jump_count(text.encode(), _p(limbs)))
         return sum(int(limbs[k]) << (64 * k) for k in range(4))
+
+    def to_text_bulk(self, states: np.ndarray, threads: int = 1, slot: int = 1408):
+        """Threaded ranmar::to_text into fixed slots -> (buffer, total bytes)."""
+        states = np.ascontiguousarray(states)
+        buf = np.zeros(len(states) * slot, np.uint8)
+        total = self.lib.ref_to_text_bulk(_p(states), len(states), _p(buf), slot, threads)
+        assert total >= 0
+        return buf, total
+
+    def from_text_bulk(self, blob: np.ndarray, offsets: np.ndarray, threads: int = 1):
+        """Threaded ranmar::from_text of texts [offsets[k], offsets[k+1]) -> (states, failures)."""
+        n = len(offsets) - 1
+        out = np.zeros(n, STATE_DTYPE)
+        bad = self.lib.ref_from_text_bulk(_p(np.ascontiguousarray(blob)),
+                                          _p(np.ascontiguousarray(offsets, np.uint64)), n,
+                                          _p(out), threads)
+        return out, bad
 
     def to_text(self, state: np.ndarray) -> str:
         buf = C.create_string_buffer(4096)

@@ -247,6 +247,49 @@ int ref_jump_batch(const RanmarState* in, std::uint64_t n, const std::uint64_t* 
     });
 }
 
+// Bulk persistence on the host, threaded: to_text of n states into per-state
+// slots of `slot` bytes (returns total bytes, or -1 if a slot is too small),
+// and from_text of n texts (count of parse failures).
+long ref_to_text_bulk(const RanmarState* s, std::uint64_t n, char* buf, long slot, int threads) {
+    std::vector<long> tot(threads > 0 ? threads : 1, 0);
+    parallel_ranges(n, threads, [&](int tid, std::uint64_t lo, std::uint64_t hi) {
+        long t = 0;
+        for (std::uint64_t k = lo; k < hi; ++k) {
+            const std::string x = ranmar::to_text(s[k]);
+            if (static_cast<long>(x.size()) > slot) {
+                t = -1;
+                break;
+            }
+            std::memcpy(buf + k * slot, x.data(), x.size());
+            t += static_cast<long>(x.size());
+        }
+        tot[static_cast<std::size_t>(tid)] = t;
+    });
+    long total = 0;
+    for (long t : tot) {
+        if (t < 0) return -1;
+        total += t;
+    }
+    return total;
+}
+
+long ref_from_text_bulk(const char* buf, const std::uint64_t* off, std::uint64_t n,
+                        RanmarState* out, int threads) {
+    std::vector<long> bad(threads > 0 ? threads : 1, 0);
+    parallel_ranges(n, threads, [&](int tid, std::uint64_t lo, std::uint64_t hi) {
+        for (std::uint64_t k = lo; k < hi; ++k) {
+            try {
+                out[k] = ranmar::from_text(std::string_view(buf + off[k], off[k + 1] - off[k]));
+            } catch (const std::invalid_argument&) {
+                ++bad[static_cast<std::size_t>(tid)];
+            }
+        }
+    });
+    long b = 0;
+    for (long x : bad) b += x;
+    return b;
+}
+
 // C4 shape: per-stream u64 sum of the 24-bit outputs and a 256-bin histogram
 // of u >> 16, streams [first, first+n) of make_streams(base, J).
 int ref_consume(const RanmarState* base, const std::uint64_t* jlimbs, std::uint64_t first,
