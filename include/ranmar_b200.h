@@ -63,6 +63,15 @@ typedef struct ranmar_gauss_state {
     uint32_t pad;
 } ranmar_gauss_state;
 
+/* ranmar::reference::FloatState (reference/float_ranmar.hpp:22-29): the
+ * classic floating-point generator, 97 doubles + c + cursors (792 B). */
+typedef struct ranmar_float_state {
+    double x[97];
+    double c;
+    int32_t i;
+    int32_t j;
+} ranmar_float_state;
+
 typedef struct ranmar_ctx ranmar_ctx;
 
 /* ------------------------------------------------------------ host, no GPU */
@@ -74,6 +83,9 @@ int ranmar_init(uint32_t seed, ranmar_state* out);
 /* Same seed expansion without the range check (BASELINE config 3 uses seed
  * 987654321, which ranmar::init rejects; documented deviation). */
 int ranmar_init_unchecked(uint32_t seed, ranmar_state* out);
+/* ranmar::reference::init_float(seed) float_ranmar.hpp:50-80 (EINVAL above
+ * 900000000): x[k] = lane/2^24, c = 362436/2^24, the float image of init. */
+int ranmar_init_float(uint32_t seed, ranmar_float_state* out);
 /* ranmar::value_of(u24)          core.hpp:75-79 (EINVAL if u24 > 2^24-1) */
 int ranmar_value_of(uint32_t u24, double* out);
 /* ranmar::parse_jump_count(text) jumpcount.hpp:16-47 (EINVAL on bad text;
@@ -121,6 +133,12 @@ int ranmar_generate_f32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t
                             float* d_out, void* stream);
 int ranmar_generate_f64_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
                             double* d_out, void* stream);
+
+/* per_stream calls of reference::step_float (float_ranmar.hpp:33-46, the
+ * classic Algorithm 1 in binary64) on each device float state; bit-identical
+ * to the integer path's outputs / 2^24. States advance in place. */
+int ranmar_generate_float_dev(ranmar_float_state* d_states, uint64_t n_streams,
+                              uint64_t per_stream, double* d_out, void* stream);
 
 /* Consume-in-kernel (no uniform is stored): per stream, the u64 sum of its
  * per_stream 24-bit outputs and a 256-bin histogram of (u >> 16);

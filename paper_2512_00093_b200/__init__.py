@@ -27,6 +27,8 @@ STATE_DTYPE = np.dtype([("lane", "<u4", (97,)), ("i", "<i4"), ("j", "<i4"), ("v"
 GAUSS_DTYPE = np.dtype([("s", STATE_DTYPE), ("saved", "<f8"), ("has_saved", "<u4"), ("pad", "<u4")])
 STATE_WORDS = 100
 GAUSS_WORDS = 104
+# ranmar::reference::FloatState (float_ranmar.hpp:22-29): 792 bytes.
+FLOAT_DTYPE = np.dtype([("x", "<f8", (97,)), ("c", "<f8"), ("i", "<i4"), ("j", "<i4")])
 
 long_lag, short_lag, word_bits = 97, 33, 24             # core.hpp:17-19
 word_mask = 0x00FFFFFF                                  # core.hpp:20
@@ -93,6 +95,8 @@ def lib() -> C.CDLL:
         "ranmar_ctx_generate_f32": (i32, [vp, vp, u64, u64, vp]),
         "ranmar_ctx_consume": (i32, [vp, vp, u64, u64, vp, vp]),
         "ranmar_gaussian_stream_f64_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_init_float": (i32, [u32, vp]),
+        "ranmar_generate_float_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_to_text_bound": (u64, [u64]),
         "ranmar_text_workspace": (sz, [u64]),
         "ranmar_to_text_dev": (i32, [vp, u64, vp, u64, vp, vp, sz, vp]),
@@ -151,6 +155,27 @@ def init_unchecked(seed: int) -> np.ndarray:
     s = np.zeros(1, STATE_DTYPE)
     _check(lib().ranmar_init_unchecked(seed, _ptr(s)))
     return s
+
+
+def init_float(seed: int) -> np.ndarray:
+    """reference::init_float (float_ranmar.hpp:50-80) -> 1-element FLOAT_DTYPE array."""
+    if not 0 <= seed < 1 << 32:
+        raise ValueError("ranmar: seed must be in [0, 900000000]")
+    f = np.zeros(1, FLOAT_DTYPE)
+    _check(lib().ranmar_init_float(seed, _ptr(f)))
+    return f
+
+
+def generate_float(fstates, per_stream: int, out=None, stream=None):
+    """per_stream calls of reference::step_float (Algorithm 1, binary64) per float
+    state (uint8 CUDA tensor [n, 792]), advanced in place -> float64 [n * per_stream]."""
+    torch = _torch()
+    n = fstates.shape[0]
+    if out is None:
+        out = torch.empty(n * per_stream, dtype=torch.float64, device="cuda")
+    _check(lib().ranmar_generate_float_dev(_dptr(fstates), n, per_stream, _dptr(out),
+                                           _stream_ptr(stream)))
+    return out
 
 
 def value_of(u24: int) -> float:

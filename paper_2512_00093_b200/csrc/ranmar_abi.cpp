@@ -32,6 +32,8 @@ cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_
                            cudaStream_t);
 cudaError_t launch_gaussian_stream(ranmar_gauss_state*, uint64_t, uint64_t, double*, uint32_t*,
                                    cudaStream_t);
+cudaError_t launch_float_gen(ranmar_float_state*, uint64_t, uint64_t, double*, uint32_t*,
+                             cudaStream_t);
 uint64_t text_bound(uint64_t);
 size_t text_workspace(uint64_t);
 cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void*, cudaStream_t);
@@ -604,6 +606,27 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
             "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_init_float(uint32_t seed, ranmar_float_state* out) {
+    ranmar_state s;
+    if (int rc = ranmar_init(seed, &s)) return rc;
+    for (int k = 0; k < 97; ++k) out->x[k] = static_cast<double>(s.lane[k]) * 0x1p-24;
+    out->c = static_cast<double>(s.v) * 0x1p-24;
+    out->i = s.i;
+    out->j = s.j;
+    return RANMAR_OK;
+}
+
+int ranmar_generate_float_dev(ranmar_float_state* d_states, uint64_t n_streams,
+                              uint64_t per_stream, double* d_out, void* stream) {
+    if (n_streams && (!d_states || (per_stream && !d_out)))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_float_gen(d_states, n_streams, per_stream, d_out, status,
+                                 static_cast<cudaStream_t>(stream)),
+            "float_gen_kernel launch");
     return RANMAR_OK;
 }
 
