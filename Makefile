@@ -12,7 +12,7 @@ OBJS := $(BUILD)/gen_kernels.o $(BUILD)/float_kernel.o $(BUILD)/consume_kernel.o
 HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh
 
 .PHONY: all lib oracle ref clean sass
-all: lib oracle facade
+all: lib oracle facade cli
 
 lib: $(LIB)
 
@@ -45,3 +45,11 @@ FACADE := tests/cpp/facade_test
 facade: $(FACADE)
 $(FACADE): tests/cpp/facade_test.cpp include/ranmar_b200.hpp $(LIB)
 	g++ -O2 -std=c++20 -Iinclude $< -L$(PKG)/lib -lranmar_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -o $@
+
+# GPU-backed CLI mirroring the reference's ranmar tool
+CLI := $(PKG)/bin/ranmar_b200
+cli: $(CLI)
+$(CLI): tools/ranmar_cli.cpp include/ranmar_b200.hpp $(LIB)
+	@mkdir -p $(dir $(CLI))
+	g++ -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -L$(PKG)/lib -lranmar_b200 \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../lib' -Wl,-rpath,/usr/local/cuda/lib64 -o $@
