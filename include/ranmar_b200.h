@@ -152,6 +152,12 @@ int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_
 int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, void* stream);
 
+/* Diagnostic: compares gaussian()'s branch-free fp64 divide / sqrt with the
+ * CUDA library's correctly rounded ones on n operand sets drawn from seed
+ * (rsq = s / 2^46); adds the number of bitwise mismatches to *d_mismatches. */
+int ranmar_fp64_selfcheck_dev(uint64_t n, uint64_t seed, unsigned long long* d_mismatches,
+                              void* stream);
+
 /* The same gaussian() calls for FEW streams with MANY calls each: one warp per
  * stream (serves the scalar RanMars-style facade). d_out[s * count + q] is
  * call q of stream s. States and cached deviates advance in place. */

@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
         "ranmar_generate_f64_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
+        "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
         "ranmar_device_status": (i32, [C.POINTER(C.c_uint32), i32]),
         "ranmar_kernel_launches": (u64, []),
         "ranmar_ctx_create": (i32, [i32, C.POINTER(vp)]),
@@ -342,6 +343,15 @@ def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
     _check(lib().ranmar_gaussian_f64_dev(_dptr(gstates), n, per_step, steps, _dptr(out),
                                          _stream_ptr(stream)))
     return out
+
+
+def fp64_selfcheck(n: int, seed: int = 1) -> int:
+    """Bitwise mismatches between gaussian()'s branch-free fp64 divide/sqrt and
+    the CUDA library's correctly rounded ones over n operand sets (expected 0)."""
+    torch = _torch()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _check(lib().ranmar_fp64_selfcheck_dev(n, seed, _dptr(bad), None))
+    return int(bad.item())
 
 
 def gaussian_stream(gstates, count: int, out=None, stream=None):

@@ -8,13 +8,14 @@
 //
 // Every gaussian() call consumes uniforms in pairs, so an atom's deviates are
 // the cached one (if has_saved) followed by (v2 fac, v1 fac) for each
-// ACCEPTED attempt pair. Each thread therefore runs one loop over attempts
-// (not one rejection loop per call, which would make a warp wait for its
-// unluckiest lane at every call): draw two uniforms, test rsq in exact integer
-// arithmetic (rsq = s / 2^46 with s = (u1 - 2^23)^2 + (u2 - 2^23)^2), and on
-// acceptance evaluate fac in fp64 and emit two deviates. A lane stops once
-// its atom has all steps * per_step deviates; the last pair's second deviate
-// becomes the cached one when the count is odd.
+// ACCEPTED attempt pair. Each thread therefore loops over attempts (not one
+// rejection loop per call, which would make a warp wait for its unluckiest
+// lane at every call): draw two uniforms, test rsq in exact integer
+// arithmetic (rsq = s / 2^46 with s = (u1 - 2^23)^2 + (u2 - 2^23)^2), and
+// collect kBatch accepted pairs; then the kBatch fp64 chains (log, divide,
+// sqrt; branch-free, gauss_math.cuh) run interleaved and emit 2 kBatch
+// deviates. The last < 2 kBatch deviates go pair by pair; the last pair's
+// second deviate becomes the cached one when the count is odd.
 //
 // The 97-word ring of each atom lives in shared memory column-major (slot s
 // of thread t at s * kGT + t): every access of a warp hits 32 distinct banks
@@ -22,51 +23,17 @@
 // with 16-B vector accesses (the 416-B records are 16-B aligned).
 #include <cstdint>
 
+#include "gauss_math.cuh"
 #include "ranmar_device.cuh"
 
 namespace rb {
 
 namespace {
 
-// gaussian()'s log: the repo convention's fixed IEEE sequence (derivation in
-// oracle/ranmar_oracle.c or_glog), with explicit round-to-nearest intrinsics
-// so nvcc cannot contract or reorder anything. The binary64 coefficients sit
-// in constant memory so DFMA reads them as operands (64-bit immediates would
-// cost a uniform move each per use inside the attempt loop).
-__constant__ double kGlogC[13] = {
-    0x1.8618618618618p-5, 0x1.af286bca1af28p-5, 0x1.e1e1e1e1e1e1ep-5, 0x1.1111111111111p-4,
-    0x1.3b13b13b13b14p-4, 0x1.745d1745d1746p-4, 0x1.c71c71c71c71cp-4, 0x1.2492492492492p-3,
-    0x1.999999999999ap-3, 0x1.5555555555555p-2,          // 1/21 .. 1/3
-    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45,         // ln2 head, tail
-    0x1.6a09e667f3bcdp+0};                               // sqrt(2)
+constexpr int kGT = 64;  // threads (atoms) per block: 24.8 KB of ring, 9 blocks/SM
+constexpr int kBatch = 4;  // accepted pairs per fp64 batch (measured best of 1..8)
 
-__device__ __forceinline__ double glog(double x) {
-    const long long b = __double_as_longlong(x);
-    int k = static_cast<int>((b >> 52) & 0x7FF) - 1023;
-    double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-    if (m > kGlogC[12]) {
-        m = __dmul_rn(m, 0.5);
-        k += 1;
-    }
-    const double f = __dsub_rn(m, 1.0);
-    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
-    const double z = __dmul_rn(s, s);
-    double p = kGlogC[0];
-#pragma unroll
-    for (int c = 1; c < 10; ++c) p = __fma_rn(p, z, kGlogC[c]);
-    const double t = __dmul_rn(s, z);
-    const double l1p = __dmul_rn(2.0, __fma_rn(t, p, s));
-    const double kd = static_cast<double>(k);
-    return __fma_rn(kd, kGlogC[10], __fma_rn(kd, kGlogC[11], l1p));
-}
-
-// v = 2 (u / 2^24) - 1, exact.
-__device__ __forceinline__ double polar_v(uint32_t u) {
-    return __dsub_rn(__dmul_rn(static_cast<double>(u), 0x1p-23), 1.0);
-}
-
-constexpr int kGT = 128;  // threads (atoms) per block
-
+template <int K>
 __global__ void __launch_bounds__(kGT)
     gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
                     uint64_t steps, double* __restrict__ out, uint32_t* status) {
@@ -117,31 +84,71 @@ __global__ void __launch_bounds__(kGT)
         has = false;
         q = 1;
     }
-    while (q < G) {
-        // attempts until one is accepted; the fp64 part then runs with the
-        // whole warp converged (every lane needs a new pair at the same call)
-        uint32_t u0, u1;
-        for (;;) {
-            uint32_t u[2];
+    // one attempt: two uniforms (core.hpp:54-66 on the ring); true when
+    // 0 < rsq < 1 holds exactly (rsq = s / 2^46)
+    auto attempt = [&](uint32_t& u0, uint32_t& u1) -> bool {
+        uint32_t u[2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {  // two uniforms (core.hpp:54-66 on the ring)
-                const int j = i >= 64 ? i - 64 : i + 33;
-                const uint32_t x = col[i * kGT] - col[j * kGT];
-                col[i * kGT] = x;
-                i = i == 0 ? 96 : i - 1;
-                v = add_mod_m(v, kStepA);
-                u[h] = (x - v) & kMask;
-            }
-            const int32_t da = static_cast<int32_t>(u[0]) - (1 << 23);
-            const int32_t db = static_cast<int32_t>(u[1]) - (1 << 23);
-            const int64_t s = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
-            u0 = u[0];
-            u1 = u[1];
-            if (s > 0 && s < (int64_t(1) << 46)) break;  // 0 < rsq < 1, exactly
+        for (int h = 0; h < 2; ++h) {
+            const int j = i >= 64 ? i - 64 : i + 33;
+            const uint32_t x = col[i * kGT] - col[j * kGT];
+            col[i * kGT] = x;
+            i = i == 0 ? 96 : i - 1;
+            v = add_mod_m(v, kStepA);
+            u[h] = (x - v) & kMask;
         }
+        const int32_t da = static_cast<int32_t>(u[0]) - (1 << 23);
+        const int32_t db = static_cast<int32_t>(u[1]) - (1 << 23);
+        const int64_t s = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
+        u0 = u[0];
+        u1 = u[1];
+        return s > 0 && s < (int64_t(1) << 46);
+    };
+    auto accept = [&](uint32_t& u0, uint32_t& u1) {
+        while (!attempt(u0, u1)) {
+        }
+    };
+    // Batches of K accepted pairs. One attempt loop collects all K (accepted
+    // pairs shift into a[], b[] in order), so a warp waits for its slowest lane
+    // once per batch rather than once per pair; then the K independent fp64
+    // chains (log, divide, sqrt) are interleaved, so the fp64 pipe sees K-fold
+    // instruction-level parallelism instead of one dependent chain per thread.
+    while (G - q >= 2 * K) {
+        uint32_t a[K], b[K];
+        for (int got = 0; got < K;) {
+            uint32_t u0, u1;
+            if (attempt(u0, u1)) {
+#pragma unroll
+                for (int k = 0; k + 1 < K; ++k) {
+                    a[k] = a[k + 1];
+                    b[k] = b[k + 1];
+                }
+                a[K - 1] = u0;
+                b[K - 1] = u1;
+                ++got;
+            }
+        }
+        double v1[K], v2[K], fac[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            v1[k] = polar_v(a[k]);
+            v2[k] = polar_v(b[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) fac[k] = polar_fac(v1[k], v2[k]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            put(__dmul_rn(v2[k], fac[k]));
+            saved = __dmul_rn(v1[k], fac[k]);  // the oracle keeps the last pair's v1 fac
+            put(saved);
+        }
+        q += 2 * K;
+    }
+    while (q < G) {
+        uint32_t u0, u1;
+        accept(u0, u1);
         const double v1 = polar_v(u0), v2 = polar_v(u1);
-        const double rsq = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
-        const double fac = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glog(rsq)), rsq));
+        const double fac = polar_fac(v1, v2);
         saved = __dmul_rn(v1, fac);
         put(__dmul_rn(v2, fac));
         if (q + 1 < G) {
@@ -168,23 +175,69 @@ __global__ void __launch_bounds__(kGT)
 
 }  // namespace
 
-cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
-                            uint64_t steps, double* d_out, uint32_t* status,
-                            cudaStream_t stream) {
-    if (n_atoms == 0 || per_step == 0 || steps == 0) return cudaSuccess;
+// Self-check of div_rn / sqrt_rn against the library's __ddiv_rn / __dsqrt_rn
+// on the operands gaussian() can produce: rsq = s / 2^46 for pseudo-random
+// s in [1, 2^46) plus the range ends and powers of two; per value the glog
+// division f / (2 + f), the fac division and the sqrt are compared bitwise.
+__global__ void fp64_selfcheck_kernel(uint64_t n, uint64_t seed,
+                                      unsigned long long* __restrict__ bad) {
+    unsigned long long miss = 0;
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;  // splitmix64
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        uint64_t s = z & ((uint64_t(1) << 46) - 1);
+        if (k < 47) s = uint64_t(1) << k;  // powers of two: f = 0 in glog
+        if (k == 47) s = (uint64_t(1) << 46) - 1;
+        if (s == 0 || s >= (uint64_t(1) << 46)) s = 1;
+        const double rsq = static_cast<double>(s) * 0x1p-46;
+        const long long b = __double_as_longlong(rsq);
+        double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+        if (m > kGlogC[12]) m = __dmul_rn(m, 0.5);
+        const double f = __dsub_rn(m, 1.0), d = __dadd_rn(2.0, f);
+        miss += __double_as_longlong(div_rn(f, d)) != __double_as_longlong(__ddiv_rn(f, d));
+        const double num = __dmul_rn(-2.0, glog(rsq));
+        const double q1 = div_rn(num, rsq), q2 = __ddiv_rn(num, rsq);
+        miss += __double_as_longlong(q1) != __double_as_longlong(q2);
+        miss += __double_as_longlong(sqrt_rn(q2)) != __double_as_longlong(__dsqrt_rn(q2));
+    }
+    if (miss) atomicAdd(bad, miss);
+}
+
+cudaError_t launch_fp64_selfcheck(uint64_t n, uint64_t seed, unsigned long long* d_bad,
+                                  cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    fp64_selfcheck_kernel<<<148 * 8, 256, 0, stream>>>(n, seed, d_bad);
+    return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
+                              uint64_t steps, double* d_out, uint32_t* status,
+                              cudaStream_t stream) {
     const int smem = 97 * kGT * 4;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gaussian_kernel,
+        cudaError_t e = cudaFuncSetAttribute(gaussian_kernel<K>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
     count_launch();
-    gaussian_kernel<<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(d_g, n_atoms, per_step,
-                                                                          steps, d_out, status);
+    gaussian_kernel<K><<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(
+        d_g, n_atoms, per_step, steps, d_out, status);
     return cudaGetLastError();
+}
+
+cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
+                            uint64_t steps, double* d_out, uint32_t* status,
+                            cudaStream_t stream) {
+    if (n_atoms == 0 || per_step == 0 || steps == 0) return cudaSuccess;
+    return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
 }
 
 }  // namespace rb

@@ -15,43 +15,12 @@
 // Output: out[s * count + q] = call q of stream s.
 #include <cstdint>
 
+#include "gauss_math.cuh"
 #include "ranmar_device.cuh"
 
 namespace rb {
 
 namespace {
-
-__constant__ double kGlogS[13] = {
-    0x1.8618618618618p-5, 0x1.af286bca1af28p-5, 0x1.e1e1e1e1e1e1ep-5, 0x1.1111111111111p-4,
-    0x1.3b13b13b13b14p-4, 0x1.745d1745d1746p-4, 0x1.c71c71c71c71cp-4, 0x1.2492492492492p-3,
-    0x1.999999999999ap-3, 0x1.5555555555555p-2,          // 1/21 .. 1/3
-    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45,         // ln2 head, tail
-    0x1.6a09e667f3bcdp+0};                               // sqrt(2)
-
-// The convention's log (oracle/ranmar_oracle.c or_glog), explicit IEEE ops.
-__device__ __forceinline__ double glog_s(double x) {
-    const long long b = __double_as_longlong(x);
-    int k = static_cast<int>((b >> 52) & 0x7FF) - 1023;
-    double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-    if (m > kGlogS[12]) {
-        m = __dmul_rn(m, 0.5);
-        k += 1;
-    }
-    const double f = __dsub_rn(m, 1.0);
-    const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
-    const double z = __dmul_rn(s, s);
-    double p = kGlogS[0];
-#pragma unroll
-    for (int c = 1; c < 10; ++c) p = __fma_rn(p, z, kGlogS[c]);
-    const double t = __dmul_rn(s, z);
-    const double l1p = __dmul_rn(2.0, __fma_rn(t, p, s));
-    const double kd = static_cast<double>(k);
-    return __fma_rn(kd, kGlogS[10], __fma_rn(kd, kGlogS[11], l1p));
-}
-
-__device__ __forceinline__ double polar_vs(uint32_t u) {
-    return __dsub_rn(__dmul_rn(static_cast<double>(u), 0x1p-23), 1.0);
-}
 
 __device__ __forceinline__ int mod97s(int64_t x) {
     int64_t r = x % 97;
@@ -158,10 +127,9 @@ __global__ void __launch_bounds__(32 * kSW)
         uint32_t at = 0;
         if (static_cast<uint32_t>(l) < cnt) {
             const uint32_t slot = (qhead + l) & (kQCap - 1);
-            const double v1 = polar_vs(qu1[w][slot]), v2 = polar_vs(qu2[w][slot]);
+            const double v1 = polar_v(qu1[w][slot]), v2 = polar_v(qu2[w][slot]);
             at = qat[w][slot];
-            const double rsq = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
-            const double fac = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glog_s(rsq)), rsq));
+            const double fac = polar_fac(v1, v2);
             g1 = __dmul_rn(v2, fac);
             g2 = __dmul_rn(v1, fac);
             const uint64_t qa = q + 2 * static_cast<uint64_t>(l);

@@ -41,6 +41,7 @@ cudaError_t launch_from_text(const char*, const uint64_t*, uint64_t, ranmar_stat
                              cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
+cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
                              const uint32_t*, cudaStream_t);
@@ -606,6 +607,14 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
             "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_fp64_selfcheck_dev(uint64_t n, uint64_t seed, unsigned long long* d_mismatches,
+                              void* stream) {
+    if (n && !d_mismatches) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_CUDA(rb::launch_fp64_selfcheck(n, seed, d_mismatches, static_cast<cudaStream_t>(stream)),
+            "fp64_selfcheck_kernel launch");
     return RANMAR_OK;
 }
 

@@ -263,7 +263,8 @@ def test_gaussian_within_one_ulp(oracle):
     exp = oracle.gaussian_fill(og, per, steps)
     d = ulp_diff(out.reshape(-1), exp.reshape(-1))
     print(f"gaussian max ulp {d.max()}, differing {np.count_nonzero(d)} of {d.size}")
-    assert d.max() <= 1  # north-star tolerance; the shared log convention gives 0
+    assert d.max() <= 1  # north-star tolerance
+    assert d.max() == 0  # and the shared log convention makes it bit-exact
     og2 = np.zeros(n, GAUSS_DTYPE)
     og2["s"] = rb.states_to_host(states)
     libm = oracle.gaussian_fill(og2, per, steps, libm_log=True)
@@ -273,6 +274,13 @@ def test_gaussian_within_one_ulp(oracle):
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
     assert gh["s"].tobytes() == og["s"].tobytes()
     assert (gh["has_saved"] == og["has_saved"]).all()
+
+
+def test_fp64_fast_paths_match_library():
+    # gaussian()'s branch-free divide / sqrt (csrc/gauss_math.cuh) against
+    # __ddiv_rn / __dsqrt_rn on 2^28 operand sets rsq = s / 2^46 (bitwise)
+    assert rb.fp64_selfcheck(1 << 28, seed=12345) == 0
+    assert rb.fp64_selfcheck(1 << 20, seed=7) == 0
 
 
 def test_gaussian_odd_count_keeps_cache(oracle):
