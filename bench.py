@@ -428,7 +428,45 @@ def run_ours(args, rank, world, local):
         extras["config5"] = {"workload": "2^24 atoms x 3 gaussian() x 100 steps per rank, fp64 out",
                              "gaussians_per_s": out5.numel() * world / (ms5 * 1e-3), "ms": ms5,
                              "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9}
-        del out5, g5, g5w
+
+        # the same 100 steps launched one MD step at a time (3 deviates per atom
+        # per launch: states stepped in place, K6), then the fused consumer
+        def timed(fn, reps):
+            g5w.copy_(g5)
+            fn()  # warm-up launch
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return max_over_ranks(e0.elapsed_time(e1), world) / reps
+
+        steps5 = C5["steps"]
+        ms_ps = timed(lambda: rb.gaussian(g5w, C5["per"], 1, out=out5[0:1], stream=stream), steps5)
+        extras["config5"]["per_step_launches"] = {
+            "ms_per_step": ms_ps, "ms_100_steps": ms_ps * steps5,
+            "gaussians_per_s": n5 * C5["per"] * world / (ms_ps * 1e-3)}
+        del out5
+        gen = torch.Generator(device=dev).manual_seed(5)
+        vel = torch.randn((n5, 3), dtype=torch.float64, device=dev, generator=gen)
+        frc = torch.zeros((n5, 3), dtype=torch.float64, device=dev)
+        typ = torch.ones(n5, dtype=torch.int32, device=dev)
+        lang = {"workload": "2^24 atoms, one stream per atom (config 5 streams), f += g1 v + "
+                            "g2 r per component, one launch per MD step"}
+        for name, noise in (("uniform", rb.NOISE_UNIFORM), ("gaussian", rb.NOISE_GAUSSIAN)):
+            gf1, gf2 = rb.langevin_factors([0.0, 1.0], 0.1, 0.005, noise=noise)
+            d1, d2 = torch.from_numpy(gf1).to(dev), torch.from_numpy(gf2).to(dev)
+            ms_l = timed(lambda: rb.langevin(g5w, vel, frc, typ, d1, d2, 1.0, noise,
+                                             stream=stream), 20)
+            # algorithmic bytes per atom-step: v 24 + f 24 read + 24 written + type 4 +
+            # state cursors/v 12 read + 12 written + 2 x 3 ring words read + 3 written
+            # (uniform: 3 uniforms; gaussian: ~3.8 uniforms, counted as 3)
+            lang[name] = {"ms_per_step": ms_l, "atoms_per_s": n5 * world / (ms_l * 1e-3),
+                          "algorithmic_GB_per_s": n5 * 136 / (ms_l * 1e-3) / 1e9}
+        extras["langevin"] = lang
+        del g5, g5w, vel, frc, typ
 
     if rank != 0:
         return

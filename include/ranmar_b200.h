@@ -152,6 +152,23 @@ int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_
 int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, void* stream);
 
+/* Fix-langevin-style per-atom consumer (no reference counterpart; SURVEY
+ * §8f rows 3-4): one stream per atom, uniforms/gaussians consumed in-kernel.
+ * For each atom a with d_mask == NULL or (d_mask[a] & groupbit) != 0, with
+ * t = d_type[a] in [0, n_types], g1 = d_gfactor1[t], g2 = d_gfactor2[t] * tsqrt:
+ *   for d = 0..2:  r = uniform() - 0.5      (RANMAR_NOISE_UNIFORM)
+ *                  r = gaussian()           (RANMAR_NOISE_GAUSSIAN)
+ *                  d_f[3a+d] = d_f[3a+d] + (g1 * d_v[3a+d] + g2 * r)
+ * every operation rounded separately. d_v, d_f are n_atoms x 3 doubles
+ * (LAMMPS v[i][d], f[i][d]); d_gfactor* hold n_types + 1 doubles. States
+ * advance in place; a type outside [0, n_types] sets status bit 2. */
+#define RANMAR_NOISE_UNIFORM 0
+#define RANMAR_NOISE_GAUSSIAN 1
+int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double* d_v,
+                        double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                        int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
+                        int32_t n_types, double tsqrt, int noise, void* stream);
+
 /* Diagnostic: compares gaussian()'s branch-free fp64 divide / sqrt with the
  * CUDA library's correctly rounded ones on n operand sets drawn from seed
  * (rsq = s / 2^46); adds the number of bitwise mismatches to *d_mismatches. */
@@ -180,7 +197,8 @@ int ranmar_from_text_dev(const char* d_text, const uint64_t* d_offsets, uint64_t
                          ranmar_state* d_states, int32_t* d_err, void* stream);
 
 /* Sticky status bits of the current device (bit 0: a kernel met a state with
- * bad cursors / v >= m). Synchronises the device. clear != 0 resets them. */
+ * bad cursors / v >= m; bit 2: ranmar_langevin_dev met an atom type outside
+ * [0, n_types]). Synchronises the device. clear != 0 resets them. */
 int ranmar_device_status(uint32_t* flags, int clear);
 
 /* Number of kernels this library has launched in this process (all devices);

@@ -82,6 +82,8 @@ class Oracle:
             "or_consume": (None, [vp, u64, u64, vp, vp]),
             "or_gaussian_fill": (None, [vp, u64, u64, u64, vp]),
             "or_glog": (C.c_double, [C.c_double]),
+            "or_langevin": (i32, [vp, u64, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32,
+                                  C.c_double, C.c_int]),
             "or_gaussian": (C.c_double, [vp]),
             "or_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
             "or_from_text": (i32, [C.c_char_p, vp]),
@@ -194,6 +196,18 @@ class Oracle:
         finally:
             flag.value = 0
         return out
+
+    def langevin(self, gstates: np.ndarray, v: np.ndarray, f: np.ndarray, types: np.ndarray,
+                 gfactor1: np.ndarray, gfactor2: np.ndarray, tsqrt: float, noise: int,
+                 mask: np.ndarray = None, groupbit: int = 1) -> int:
+        """The repo's fix-langevin-style consumer: f (n x 3) updated in place,
+        gstates advanced; returns 1 if an atom type was out of range."""
+        for a in (v, f, types, gfactor1, gfactor2) + ((mask,) if mask is not None else ()):
+            assert a.flags["C_CONTIGUOUS"]
+        assert v.dtype == np.float64 and f.dtype == np.float64 and types.dtype == np.int32
+        return self.lib.or_langevin(_p(gstates), len(gstates), _p(v), _p(f), _p(types),
+                                    None if mask is None else _p(mask), groupbit, _p(gfactor1),
+                                    _p(gfactor2), len(gfactor1) - 1, tsqrt, noise)
 
     def glog(self, x: float) -> float:
         return self.lib.or_glog(x)

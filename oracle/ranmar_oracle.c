@@ -441,6 +441,35 @@ void or_gaussian_fill(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step, ui
                 out[(st * n_atoms + a) * per_step + c] = or_gaussian(&g[a]);
 }
 
+/* Repo-defined fix-langevin-style consumer (no
+ * reference counterpart, LAMMPS is not in the container). One stream per atom;
+ * atoms outside the group draw nothing. Every operation rounds separately
+ * (-ffp-contract=off); the device kernel langevin_kernel performs the same
+ * sequence. noise 0: r = uniform() - 0.5; noise 1: r = gaussian(). */
+int or_langevin(or_gauss_state* g, uint64_t n_atoms, const double* v, double* f,
+                const int32_t* type, const int32_t* mask, int32_t groupbit,
+                const double* gfactor1, const double* gfactor2, int32_t n_types, double tsqrt,
+                int noise) {
+    int bad_type = 0;
+    for (uint64_t a = 0; a < n_atoms; ++a) {
+        if (mask && !(mask[a] & groupbit)) continue;
+        const int32_t t = type[a];
+        if (t < 0 || t > n_types) {
+            bad_type = 1;
+            continue;
+        }
+        const double g1 = gfactor1[t];
+        const double g2 = gfactor2[t] * tsqrt;
+        for (int d = 0; d < 3; ++d) {
+            const double r = noise ? or_gaussian(&g[a])
+                                   : (double)or_step(&g[a].s) * 0x1p-24 - 0.5;
+            const double fd = g1 * v[3 * a + d] + g2 * r;
+            f[3 * a + d] = f[3 * a + d] + fd;
+        }
+    }
+    return bad_type;
+}
+
 /* ---------------------------------------------------------- text state --- */
 
 /* serialize.hpp:21-40: "ranmar24 v1", 1-based cursors, v, 97 lanes. */

@@ -105,6 +105,12 @@ typedef struct or_gauss_state {
 double or_glog(double x);
 extern int or_gauss_use_libm_log;
 double or_gaussian(or_gauss_state* g);
+/* Repo-defined fix-langevin-style consumer; returns 1 if an atom type was out
+ * of [0, n_types] (that atom is skipped). */
+int or_langevin(or_gauss_state* g, uint64_t n_atoms, const double* v, double* f,
+                const int32_t* type, const int32_t* mask, int32_t groupbit,
+                const double* gfactor1, const double* gfactor2, int32_t n_types, double tsqrt,
+                int noise);
 void or_gaussian_fill(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step, uint64_t steps,
                       double* out /* [step][atom][per_step] */);
 

@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
         "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
         "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
+        "ranmar_langevin_dev": (i32, [vp, u64, vp, vp, vp, vp, i32, vp, vp, i32, C.c_double,
+                                      i32, vp]),
         "ranmar_device_status": (i32, [C.POINTER(C.c_uint32), i32]),
         "ranmar_kernel_launches": (u64, []),
         "ranmar_ctx_create": (i32, [i32, C.POINTER(vp)]),
@@ -343,6 +345,44 @@ def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
     _check(lib().ranmar_gaussian_f64_dev(_dptr(gstates), n, per_step, steps, _dptr(out),
                                          _stream_ptr(stream)))
     return out
+
+
+NOISE_UNIFORM, NOISE_GAUSSIAN = 0, 1
+
+
+def langevin_factors(mass, t_period: float, dt: float, noise: int = NOISE_UNIFORM,
+                     boltz: float = 1.0, mvv2e: float = 1.0, ftm2v: float = 1.0):
+    """Per-type (gfactor1, gfactor2) of a Langevin thermostat (Schneider-Stoll
+    form as used by fix langevin): drag -m / damp and a random force whose
+    variance matches 2 m kB T / (damp dt) — 24 kB T m / (damp dt) for the
+    uniform(-1/2, 1/2) noise (variance 1/12), 2 kB T m / (damp dt) for
+    gaussian noise. mass is indexed by type (entry 0 unused in LAMMPS)."""
+    m = np.asarray(mass, dtype=np.float64)
+    c = 24.0 if noise == NOISE_UNIFORM else 2.0
+    g1 = -m / t_period / ftm2v
+    g2 = np.sqrt(m) * np.sqrt(c * boltz / t_period / dt / mvv2e) / ftm2v
+    return np.ascontiguousarray(g1), np.ascontiguousarray(g2)
+
+
+def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int = NOISE_UNIFORM,
+             mask=None, groupbit: int = 1, stream=None):
+    """Fix-langevin-style consumer on CUDA tensors: for atoms in the group,
+    f[a, d] += gfactor1[t] * v[a, d] + gfactor2[t] * tsqrt * r with
+    r = uniform() - 0.5 or gaussian() from atom a's stream (ranmar_langevin_dev).
+    v, f: float64 [n, 3]; types: int32 [n]; gfactor*: float64 [n_types + 1]."""
+    n = gstates.shape[0]
+    for t, dt in ((v, "float64"), (f, "float64"), (gfactor1, "float64"), (gfactor2, "float64")):
+        if str(t.dtype) != "torch." + dt or not t.is_contiguous():
+            raise ValueError("langevin: v, f, gfactor1, gfactor2 must be contiguous float64")
+    if tuple(v.shape) != (n, 3) or tuple(f.shape) != (n, 3) or types.shape[0] != n:
+        raise ValueError("langevin: v, f must be [n_atoms, 3] and types [n_atoms]")
+    if gfactor1.shape != gfactor2.shape:
+        raise ValueError("langevin: gfactor1 and gfactor2 differ in length")
+    _check(lib().ranmar_langevin_dev(_dptr(gstates), n, _dptr(v), _dptr(f), _dptr(types),
+                                     None if mask is None else _dptr(mask), groupbit,
+                                     _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
+                                     float(tsqrt), noise, _stream_ptr(stream)))
+    return f
 
 
 def fp64_selfcheck(n: int, seed: int = 1) -> int:

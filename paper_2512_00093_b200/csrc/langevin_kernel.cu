@@ -1,0 +1,180 @@
+// K6: consumers that advance a state by only a FEW outputs per launch
+// (sm_100a): the fix-langevin-style per-atom force update (SURVEY.md §8f rows
+// 3-4) and gaussian() with few deviates per atom per launch (the per-step
+// launch mode of config 5).
+//
+// A launch that draws ~3-10 outputs from a stream touches ~3-10 ring words at
+// the read cursor i and as many at j = i - 64 (mod 97), plus the cursors and
+// v. Staging the whole 97-word ring (K4) would move 832 B per atom for that;
+// here each thread steps its state IN PLACE in global memory (core.hpp:54-66
+// on the record itself): the touched words come through L1 (a few 32-B
+// sectors per atom), and only they are written back. Within a launch a word
+// written at step n is read again at step n + 33 at the earliest, by the same
+// thread, so in-place stepping is exact.
+//
+// Langevin force (repo convention; the reference has no consumer, LAMMPS is
+// not in the container): for each atom a in the group, type t = type[a],
+//   g1 = gfactor1[t], g2 = gfactor2[t] * tsqrt,
+//   for d = 0, 1, 2:  r = uniform() - 0.5   (noise 0, LAMMPS' default form)
+//                     r = gaussian()        (noise 1)
+//                     f[a][d] = f[a][d] + (g1 * v[a][d] + g2 * r)
+// every operation rounded separately (oracle/ranmar_oracle.c or_langevin).
+// Atoms outside the group (mask[a] & groupbit == 0) draw nothing.
+#include <cstdint>
+
+#include "gauss_math.cuh"
+#include "ranmar_device.cuh"
+
+namespace rb {
+
+namespace {
+
+// One stream stepped in place in global memory.
+struct InPlace {
+    uint32_t* lane;
+    int i, j;
+    uint32_t v;
+
+    __device__ __forceinline__ uint32_t next() {
+        const uint32_t x = (lane[i] - lane[j]) & kMask;
+        lane[i] = x;
+        i = i == 0 ? 96 : i - 1;
+        j = j == 0 ? 96 : j - 1;
+        v = add_mod_m(v, kStepA);
+        return (x - v) & kMask;
+    }
+};
+
+// gaussian() on an in-place stream (oracle or_gaussian; exact integer test).
+__device__ __forceinline__ double gauss_next(InPlace& st, double& saved, bool& has) {
+    if (has) {
+        has = false;
+        return saved;
+    }
+    uint32_t u0, u1;
+    for (;;) {
+        u0 = st.next();
+        u1 = st.next();
+        const int32_t da = static_cast<int32_t>(u0) - (1 << 23);
+        const int32_t db = static_cast<int32_t>(u1) - (1 << 23);
+        const int64_t s = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
+        if (s > 0 && s < (int64_t(1) << 46)) break;
+    }
+    const double v1 = polar_v(u0), v2 = polar_v(u1);
+    const double fac = polar_fac(v1, v2);
+    saved = __dmul_rn(v1, fac);
+    has = true;
+    return __dmul_rn(v2, fac);
+}
+
+template <bool kGauss>
+__global__ void __launch_bounds__(256)
+    langevin_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms,
+                    const double* __restrict__ vel, double* __restrict__ force,
+                    const int32_t* __restrict__ type, const int32_t* __restrict__ mask,
+                    int32_t groupbit, const double* __restrict__ gf1,
+                    const double* __restrict__ gf2, int32_t n_types, double tsqrt,
+                    uint32_t* status) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_atoms) return;
+    if (mask != nullptr && (mask[a] & groupbit) == 0) return;
+    const int32_t t = type[a];
+    if (t < 0 || t > n_types) {
+        atomicOr(status, kStatusBadType);
+        return;
+    }
+    ranmar_gauss_state* gs = g + a;
+    InPlace st{gs->s.lane, gs->s.i, gs->s.j, gs->s.v};
+    if (!state_ok(st.i, st.j, st.v)) {
+        atomicOr(status, kStatusBadState);
+        return;
+    }
+    double saved = 0.0;
+    bool has = false;
+    if (kGauss) {
+        saved = gs->saved;
+        has = gs->has_saved != 0;
+    }
+    const double g1 = gf1[t];
+    const double g2 = __dmul_rn(gf2[t], tsqrt);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double r;
+        if (kGauss) {
+            r = gauss_next(st, saved, has);
+        } else {
+            r = __dsub_rn(__dmul_rn(static_cast<double>(st.next()), 0x1p-24), 0.5);
+        }
+        const double fd = __dadd_rn(__dmul_rn(g1, vel[3 * a + d]), __dmul_rn(g2, r));
+        force[3 * a + d] = __dadd_rn(force[3 * a + d], fd);
+    }
+    gs->s.i = st.i;
+    gs->s.j = st.j;
+    gs->s.v = st.v;
+    if (kGauss) {
+        gs->saved = saved;
+        gs->has_saved = has ? 1u : 0u;
+    }
+}
+
+// gaussian() with few deviates per atom per launch: the same calls, output
+// layout and state semantics as gaussian_kernel (gauss_kernel.cu), stepping
+// the state in place.
+__global__ void __launch_bounds__(256)
+    gaussian_inplace_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms,
+                            uint64_t per_step, uint64_t steps, double* __restrict__ out,
+                            uint32_t* status) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_atoms) return;
+    ranmar_gauss_state* gs = g + a;
+    InPlace st{gs->s.lane, gs->s.i, gs->s.j, gs->s.v};
+    if (!state_ok(st.i, st.j, st.v)) {
+        atomicOr(status, kStatusBadState);
+        return;
+    }
+    double saved = gs->saved;
+    bool has = gs->has_saved != 0;
+    for (uint64_t s = 0; s < steps; ++s) {
+        double* o = out + (s * n_atoms + a) * per_step;
+        for (uint64_t c = 0; c < per_step; ++c) st_cs(o + c, gauss_next(st, saved, has));
+    }
+    gs->s.i = st.i;
+    gs->s.j = st.j;
+    gs->s.v = st.v;
+    gs->saved = saved;
+    gs->has_saved = has ? 1u : 0u;
+}
+
+}  // namespace
+
+cudaError_t launch_langevin(ranmar_gauss_state* d_g, uint64_t n_atoms, const double* d_v,
+                            double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                            int32_t groupbit, const double* d_gf1, const double* d_gf2,
+                            int32_t n_types, double tsqrt, int gauss, uint32_t* status,
+                            cudaStream_t stream) {
+    if (n_atoms == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((n_atoms + 255) / 256);
+    count_launch();
+    if (gauss)
+        langevin_kernel<true><<<blocks, 256, 0, stream>>>(d_g, n_atoms, d_v, d_f, d_type, d_mask,
+                                                          groupbit, d_gf1, d_gf2, n_types, tsqrt,
+                                                          status);
+    else
+        langevin_kernel<false><<<blocks, 256, 0, stream>>>(d_g, n_atoms, d_v, d_f, d_type, d_mask,
+                                                           groupbit, d_gf1, d_gf2, n_types, tsqrt,
+                                                           status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gaussian_inplace(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
+                                    uint64_t steps, double* d_out, uint32_t* status,
+                                    cudaStream_t stream) {
+    if (n_atoms == 0 || per_step == 0 || steps == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((n_atoms + 255) / 256);
+    count_launch();
+    gaussian_inplace_kernel<<<blocks, 256, 0, stream>>>(d_g, n_atoms, per_step, steps, d_out,
+                                                        status);
+    return cudaGetLastError();
+}
+
+}  // namespace rb

@@ -41,6 +41,9 @@ cudaError_t launch_from_text(const char*, const uint64_t*, uint64_t, ranmar_stat
                              cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
+cudaError_t launch_langevin(ranmar_gauss_state*, uint64_t, const double*, double*, const int32_t*,
+                            const int32_t*, int32_t, const double*, const double*, int32_t, double,
+                            int, uint32_t*, cudaStream_t);
 cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
@@ -607,6 +610,23 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
             "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double* d_v,
+                        double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                        int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
+                        int32_t n_types, double tsqrt, int noise, void* stream) {
+    if (noise != RANMAR_NOISE_UNIFORM && noise != RANMAR_NOISE_GAUSSIAN)
+        return fail(RANMAR_EINVAL, "ranmar_langevin_dev: noise must be RANMAR_NOISE_*");
+    if (n_types < 0) return fail(RANMAR_EINVAL, "ranmar_langevin_dev: n_types < 0");
+    if (n_atoms && (!d_g || !d_v || !d_f || !d_type || !d_gfactor1 || !d_gfactor2))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_langevin(d_g, n_atoms, d_v, d_f, d_type, d_mask, groupbit, d_gfactor1,
+                                d_gfactor2, n_types, tsqrt, noise == RANMAR_NOISE_GAUSSIAN, status,
+                                static_cast<cudaStream_t>(stream)),
+            "langevin_kernel launch");
     return RANMAR_OK;
 }
 

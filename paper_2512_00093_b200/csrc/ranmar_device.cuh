@@ -35,6 +35,7 @@ void count_launch(int n = 1);
 // Status bits OR-ed into the library's device status word.
 constexpr uint32_t kStatusBadState = 1u;          // cursor separation / range violated
 constexpr uint32_t kStatusInternal = 2u;          // an internal invariant failed (bug)
+constexpr uint32_t kStatusBadType = 4u;           // langevin: an atom type outside [0, n_types]
 
 static_assert(sizeof(ranmar_state) == 400, "ranmar_state must match ranmar::RanmarState");
 

@@ -225,3 +225,37 @@ def test_gaussian_log_convention_is_a_good_log(oracle):
     assert worst <= 2
     for x in (2.0**-46, 0.5, 0.999999999, 1e-10, 0.7071067811865476, 0.7071067811865475):
         assert abs(oracle.glog(x) - math.log(x)) <= 2 * math.ulp(math.log(x))
+
+
+def test_langevin_convention_statistics(oracle):
+    # The repo's fix-langevin-style consumer (or_langevin): with v = 0 the force
+    # is pure noise, f = g2 r. With rb.langevin_factors the uniform form
+    # (variance 24/12) and the gaussian form (variance 2) both give the
+    # fluctuation-dissipation variance 2 m kB T / (damp dt).
+    import paper_2512_00093_b200 as rb
+    from oracle.bind import GAUSS_DTYPE
+    n = 20000
+    mass, damp, dt, temp = 2.5, 0.2, 0.004, 1.7
+    target = 2 * mass * temp / (damp * dt)
+    for noise in (rb.NOISE_UNIFORM, rb.NOISE_GAUSSIAN):
+        g = np.zeros(n, GAUSS_DTYPE)
+        g["s"] = oracle.make_streams(oracle.init(7), 2**50, n)
+        gf1, gf2 = rb.langevin_factors([0.0, mass], damp, dt, noise=noise)
+        v = np.zeros((n, 3))
+        f = np.zeros((n, 3))
+        assert oracle.langevin(g, v, f, np.ones(n, np.int32), gf1, gf2, np.sqrt(temp), noise) == 0
+        assert abs(f.mean()) < 0.05 * np.sqrt(target)
+        assert abs(f.var() / target - 1) < 0.03
+    # drag: with zero temperature the force is exactly gfactor1 * v
+    g = np.zeros(8, GAUSS_DTYPE)
+    g["s"] = oracle.make_streams(oracle.init(7), 2**50, 8)
+    v = np.arange(24, dtype=np.float64).reshape(8, 3)
+    f = np.zeros((8, 3))
+    gf1, gf2 = rb.langevin_factors([0.0, mass], damp, dt)
+    oracle.langevin(g, v, f, np.ones(8, np.int32), gf1, gf2, 0.0, rb.NOISE_UNIFORM)
+    assert (f == gf1[1] * v).all()
+    # atoms outside the group draw nothing
+    g2 = g.copy()
+    assert oracle.langevin(g2, v, f, np.ones(8, np.int32), gf1, gf2, 1.0, 0,
+                           mask=np.zeros(8, np.int32), groupbit=1) == 0
+    assert g2.tobytes() == g.tobytes()

@@ -8,5 +8,5 @@ tail -1 gpurun_out/bench.log | python3 -c "
 import json,sys; d=json.loads(sys.stdin.read())
 print('value', d['value'], 'ms', d['ms_per_step'], 'frac', d['roofline']['frac'], 'clocks', d['clocks'])
 print('e2e', d['e2e']['value'], 'cpu', d['cpu_baseline']['value'])
-for k in ('config3','config4','config5','persistence'): print(k, d.get(k))"
+for k in ('config3','config4','config5','langevin','persistence'): print(k, d.get(k))"
 tail -1 gpurun_out/bench_ref.log | cut -c1-300
