@@ -1,0 +1,80 @@
+"""BASELINE configs 4 and 5 at their FULL sizes, and a generate call whose
+output passes 2^32 elements (64-bit indexing), checked through
+size-independent properties and spot streams recomputed by the oracle
+(each spot stream's start is make_streams(seed, J, 1, first=k), i.e. the
+reference's jump_state(s0, k J), jump.hpp:121)."""
+import numpy as np
+import pytest
+
+import paper_2512_00093_b200 as rb
+from oracle.bind import GAUSS_DTYPE
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU-only module
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def test_config4_full(oracle):
+    # 2^20 streams x 2^20 uniforms consumed (make_streams(42, 2^64))
+    n, per, j = 1 << 20, 1 << 20, 2**64
+    d = rb.make_streams(42, j, n)
+    sums, hist = rb.consume(d, per)
+    sums = sums.cpu().numpy().view(np.uint64)
+    hist = hist.cpu().numpy().view(np.uint32)
+    assert int(hist.astype(np.uint64).sum()) == n * per
+    assert (hist.sum(axis=1, dtype=np.uint64) == per).all()
+    mean = sums.astype(np.float64).mean() / per  # uniform on [0, 2^24): mean ~ 2^23
+    assert abs(mean / 2**23 - 1) < 1e-4
+    base = oracle.init(42)
+    states = d.cpu().numpy()
+    for k in (0, 1, 4097, (1 << 19) + 7, n - 1):
+        s = oracle.make_streams(base, j, 1, first=k)
+        es, eh = oracle.consume(s, per)
+        assert sums[k] == es[0] and (hist[k] == eh[0]).all(), k
+        assert states[k].tobytes() == s.tobytes(), k  # advanced by exactly 2^20 steps
+
+
+def test_config5_full(oracle):
+    # 2^24 atoms x 3 gaussian() x 100 steps in one launch (40 GB of fp64 out)
+    n, per, steps, j = 1 << 24, 3, 100, 2**50
+    d = rb.make_streams(7, j, n)
+    g = rb.gauss_states_from(d)
+    del d
+    out = rb.gaussian(g, per, steps)
+    assert torch.isfinite(out).all()
+    base = oracle.init(7)
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    for k in (0, 12345, (1 << 23) + 1, n - 1):
+        og = np.zeros(1, GAUSS_DTYPE)
+        og["s"] = oracle.make_streams(base, j, 1, first=k)
+        exp = oracle.gaussian_fill(og, per, steps)[:, 0, :]
+        got = out[:, k, :].cpu().numpy()
+        assert got.tobytes() == exp.tobytes(), k
+        assert gh[k].tobytes() == og[0].tobytes(), k
+    # moments of all 5.0e9 deviates (double accumulation on the device)
+    m1 = out.mean(dtype=torch.float64).item()
+    m2 = (out * out).mean(dtype=torch.float64).item()
+    assert abs(m1) < 1e-4 and abs(m2 - 1) < 1e-4
+
+
+def test_generate_beyond_2_32_outputs(oracle):
+    # 8192 streams x (2^19 + 3) u32 = 2^32 + 24,576 outputs: the tails of the
+    # last streams sit above element 2^32
+    n, per, j = 8192, (1 << 19) + 3, 2**40
+    d = rb.make_streams(12345, j, n)
+    out = rb.generate(d, per, "u32")
+    assert out.numel() == n * per > 2**32
+    base = oracle.init(12345)
+    states = d.cpu().numpy()
+    for k in (0, 4095, n - 2, n - 1):
+        s = oracle.make_streams(base, j, 1, first=k)
+        tail0 = per - 40
+        head = out[k * per: k * per + 40].cpu().numpy().view(np.uint32)
+        tail = out[k * per + tail0: (k + 1) * per].cpu().numpy().view(np.uint32)
+        assert (head == oracle.step_n(s.copy(), 40)).all(), k
+        t = oracle.jump_state(s, tail0)
+        assert (tail == oracle.step_n(t, 40)).all(), k
+        oracle.step_n(s, per)  # step() leaves the ring rotated (jump_state would renormalise)
+        assert states[k].tobytes() == s.tobytes(), k
