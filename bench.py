@@ -202,6 +202,53 @@ def cpu_reference_text(states: np.ndarray):
             "sample": f"{len(states)} states"}
 
 
+def cpu_reference_extras():
+    """Bounded samples of configs 3-5 and persistence on the host cores with
+    the reference's own code (oracle/_ref); config 5 has no reference
+    counterpart (gaussian() is repo-defined), so its line times the oracle
+    port on one core. A few seconds in total."""
+    from oracle.bind import GAUSS_DTYPE, Oracle, Reference, reference_available
+    if not reference_available():
+        return None
+    ref, orc, threads = Reference(), Oracle(), os.cpu_count() or 1
+
+    def best(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    ex = {}
+    base3 = orc.init(C3["seed"], checked=False)  # init.hpp:19-20 rejects this seed; see DESIGN §5
+    lat = best(lambda: ref.jump_state(base3, C3["j"]), 5)
+    n3 = 64 * threads
+    starts = best(lambda: ref.stream_starts(base3, C3["j"], 0, n3, threads), 2)
+    batch_in = ref.stream_starts(base3, C3["j"], 0, n3, threads)
+    jb = best(lambda: ref.jump_batch(batch_in, C3["j"], threads), 2)
+    ex["config3"] = {"jump_state_latency_ms_1core": lat * 1e3,
+                     "stream_starts_per_s": n3 / starts, "batched_jump_state_per_s": n3 / jb,
+                     "cores": threads, "sample": f"k in [0, {n3}) at J = 2^120"}
+    n4, per4 = 16 * threads, C4["per"]
+    base4 = ref.init(C4["seed"])
+    t4 = best(lambda: ref.consume(base4, C4["j"], 0, n4, per4, threads), 2)
+    ex["config4"] = {"uniforms_per_s": n4 * per4 / t4, "cores": threads,
+                     "sample": f"streams [0, {n4}) x 2^20 consumed (make_streams + step + sum + hist)"}
+    n5 = 4096
+    g5 = np.zeros(n5, GAUSS_DTYPE)
+    g5["s"] = orc.make_streams(orc.init(C5["seed"]), C5["j"], n5)
+
+    def run5():
+        g = g5.copy()
+        orc.gaussian_fill(g, C5["per"], C5["steps"])
+    t5 = best(run5, 2)
+    ex["config5"] = {"gaussians_per_s": n5 * C5["per"] * C5["steps"] / t5, "cores": 1,
+                     "kind": "port", "sample": f"{n5} atoms x 3 x 100 gaussian() (oracle C port)"}
+    ex["persistence"] = cpu_reference_text(ref.stream_starts(base3, C3["j"], 0, 16384, threads))
+    return ex
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -215,6 +262,9 @@ def run_reference_arm(args, rank, world):
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "uniforms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    extras = cpu_reference_extras()
+    if extras:
+        line.update(extras)
     print(json.dumps(line), flush=True)
 
 
