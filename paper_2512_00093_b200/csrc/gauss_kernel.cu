@@ -38,6 +38,9 @@ __global__ void __launch_bounds__(kGT)
     gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
                     uint64_t steps, double* __restrict__ out, uint32_t* status) {
     extern __shared__ uint32_t ring[];  // [97][kGT]
+    // shared-window address of the ring, taken before any divergence so it stays
+    // a uniform register and every ring access is one [R + UR] LDS/STS
+    const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
     const int t = threadIdx.x;
     const uint64_t atom = static_cast<uint64_t>(blockIdx.x) * kGT + t;
     if (atom >= n_atoms) return;
@@ -60,8 +63,13 @@ __global__ void __launch_bounds__(kGT)
         }
         ring[96 * kGT + t] = gs->s.lane[96];
     }
-    uint32_t* col = ring + t;
-    int i = i0;  // cursor; j = i - 64 mod 97
+    // cursors as byte offsets into the ring: slot s of this thread at 4 t + 4 kGT s.
+    // Stepping down with wraparound is one VIADDMNMX: min(a - 4 kGT, top) (unsigned:
+    // a < 4 kGT, i.e. slot 0, wraps to a huge value and yields top = slot 96).
+    constexpr uint32_t kSlot = 4 * kGT;
+    const uint32_t top = 4 * t + 96 * kSlot;
+    uint32_t ai = 4 * t + i0 * kSlot;
+    uint32_t aj = 4 * t + (i0 >= 64 ? i0 - 64 : i0 + 33) * kSlot;
     uint32_t v = v0;
     double saved = gs->saved;
     bool has = gs->has_saved != 0;
@@ -90,10 +98,13 @@ __global__ void __launch_bounds__(kGT)
         uint32_t u[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int j = i >= 64 ? i - 64 : i + 33;
-            const uint32_t x = col[i * kGT] - col[j * kGT];
-            col[i * kGT] = x;
-            i = i == 0 ? 96 : i - 1;
+            uint32_t xa, xb;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(xa) : "r"(rbase + ai));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(xb) : "r"(rbase + aj));
+            const uint32_t x = xa - xb;
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rbase + ai), "r"(x) : "memory");
+            ai = min(ai - kSlot, top);
+            aj = min(aj - kSlot, top);
             v = add_mod_m(v, kStepA);
             u[h] = (x - v) & kMask;
         }
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(kGT)
             dst[qq] = make_uint4(ring[(4 * qq + 0) * kGT + t] & kMask, ring[(4 * qq + 1) * kGT + t] & kMask,
                                  ring[(4 * qq + 2) * kGT + t] & kMask, ring[(4 * qq + 3) * kGT + t] & kMask);
     }
+    const int i = static_cast<int>((ai - 4 * t) / kSlot);
     *reinterpret_cast<uint4*>(gs->s.lane + 96) =
         make_uint4(ring[96 * kGT + t] & kMask, static_cast<uint32_t>(i),
                    static_cast<uint32_t>(i >= 64 ? i - 64 : i + 33), v);
