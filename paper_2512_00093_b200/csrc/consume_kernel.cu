@@ -35,9 +35,20 @@ __device__ __forceinline__ int mod97c(int64_t x) {
     return static_cast<int>(r < 0 ? r + 97 : r);
 }
 
-__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u) {
-    // byte address of bin u >> 16 in this thread's column: (bin >> 1) * 4 kCT + (bin & 1) * 2
-    const uint32_t a = (hb + (u >> 17) * (4 * kCT)) | ((u >> 15) & 2u);
+// Byte address of bin u >> 16 in this thread's column, (bin >> 1) 4 kCT + (bin & 1) 2,
+// written as bin 2 kCT + (bin & 1) kHalfFix with kHalfFix = 2 - 2 kCT: SHF, LOP3 and
+// two IMADs (the second multiplier comes in as a kernel argument so ptxas keeps
+// the IMAD instead of turning it into a compare and two selects).
+__device__ __forceinline__ uint32_t hist_addr(uint32_t hb, uint32_t u, uint32_t half_fix) {
+    const uint32_t bin = u >> 16;
+    const uint32_t a = hb + bin * (2 * kCT);
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(bin & 1u), "r"(half_fix), "r"(a));
+    return r;
+}
+
+__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u, uint32_t hf) {
+    const uint32_t a = hist_addr(hb, u, hf);
     uint32_t c;
     asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(a));
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(c + 1) : "memory");
@@ -66,9 +77,9 @@ __device__ __forceinline__ void flush(uint32_t* col, uint32_t* __restrict__ gh, 
 // load -> add -> store latency is paid once per pair. If both land in the
 // same counter, both loads saw the same value and the second store (v + 2)
 // overwrites the first (v + 1).
-__device__ __forceinline__ void hist_add2(uint32_t hb, uint32_t u1, uint32_t u2) {
-    const uint32_t a1 = (hb + (u1 >> 17) * (4 * kCT)) | ((u1 >> 15) & 2u);
-    const uint32_t a2 = (hb + (u2 >> 17) * (4 * kCT)) | ((u2 >> 15) & 2u);
+__device__ __forceinline__ void hist_add2(uint32_t hb, uint32_t u1, uint32_t u2, uint32_t hf) {
+    const uint32_t a1 = hist_addr(hb, u1, hf);
+    const uint32_t a2 = hist_addr(hb, u2, hf);
     uint32_t c1, c2;
     asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c1) : "r"(a1));
     asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c2) : "r"(a2));
@@ -80,7 +91,7 @@ template <int S>
 struct Body {
     // steps at compile-time slots S and S + 1, then the rest of the body
     static __device__ __forceinline__ void run(uint32_t (&X)[97], uint32_t& V, uint32_t& s32,
-                                               uint32_t hb) {
+                                               uint32_t hb, uint32_t hf) {
         X[S] -= X[(S + 64) % 97];
         V = add_mod_m(V, kStepA);
         const uint32_t u1 = (X[S] - V) & kMask;
@@ -88,25 +99,26 @@ struct Body {
         V = add_mod_m(V, kStepA);
         const uint32_t u2 = (X[S + 1] - V) & kMask;
         s32 += u1 + u2;
-        hist_add2(hb, u1, u2);
-        Body<S + 2>::run(X, V, s32, hb);
+        hist_add2(hb, u1, u2, hf);
+        Body<S + 2>::run(X, V, s32, hb, hf);
     }
 };
 template <>
 struct Body<96> {  // the 97th step alone
     static __device__ __forceinline__ void run(uint32_t (&X)[97], uint32_t& V, uint32_t& s32,
-                                               uint32_t hb) {
+                                               uint32_t hb, uint32_t hf) {
         X[96] -= X[63];
         V = add_mod_m(V, kStepA);
         const uint32_t u = (X[96] - V) & kMask;
         s32 += u;
-        hist_add(hb, u);
+        hist_add(hb, u, hf);
     }
 };
 
 __global__ void __launch_bounds__(kCT, 1)
     consume_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
-                   uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status) {
+                   uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status,
+                   uint32_t half_fix) {
     extern __shared__ uint32_t hsm[];  // [kRows][kCT]
     const int t = threadIdx.x;
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kCT + t;
@@ -137,7 +149,7 @@ __global__ void __launch_bounds__(kCT, 1)
     int since = 0;
     for (uint64_t b = 0; b < bodies; ++b) {
         uint32_t s32 = 0;  // 97 x (2^24 - 1) < 2^31
-        Body<0>::run(X, V, s32, hb);
+        Body<0>::run(X, V, s32, hb, half_fix);
         sum64 += s32;
         if (++since == kBodiesPerFlush) {
             flush(col, gh, flushed, true);
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(kCT, 1)
         V = add_mod_m(V, kStepA);
         const uint32_t u = (L[s] - V) & kMask;
         sum64 += u;
-        hist_add(hb, u);
+        hist_add(hb, u, half_fix);
     }
     // slot s <-> ring position (i0 - s) mod 97, whatever N is
 #pragma unroll
@@ -182,7 +194,7 @@ cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t 
     const uint64_t blocks = (n_streams + kCT - 1) / kCT;
     count_launch();
     consume_kernel<<<static_cast<unsigned>(blocks), kCT, kConsumeSmem, stream>>>(
-        d_states, n_streams, per_stream, d_sums, d_hist, status);
+        d_states, n_streams, per_stream, d_sums, d_hist, status, static_cast<uint32_t>(2 - 2 * kCT));
     return cudaGetLastError();
 }
 
