@@ -85,6 +85,20 @@ def test_jump_large_and_additive(oracle):
     assert torch.equal(d2, rb.jump_dev(d, 12345))
 
 
+def test_jump_commutes_with_stepping(oracle):
+    # test_jump.cpp "jumping commutes with stepping", on the device: step n then
+    # jump J == jump J then step n (compared through the next outputs, since a
+    # stepped ring is rotated and a jumped one renormalised)
+    base = random_states(64, 11, oracle)
+    for n, j in ((1, 2**40), (97, 12345), (1000, 2**120 - 1)):
+        a = rb.states_to_device(base)
+        rb.generate(a, n, "u32")
+        a = rb.jump_dev(a, j)
+        b = rb.jump_dev(rb.states_to_device(base), j)
+        rb.generate(b, n, "u32")
+        assert torch.equal(rb.generate(a, 500, "u32"), rb.generate(b, 500, "u32")), (n, j)
+
+
 def test_make_streams_golden(refvec):
     for case in refvec["make_streams"]:
         got = rb.states_to_host(rb.make_streams(case["seed"], int(case["j"]), len(case["states"])))
