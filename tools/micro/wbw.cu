@@ -12,6 +12,22 @@ __global__ void v4(float4* p, size_t n4) {
         asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + i), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
     }
 }
+__global__ void v4c(float4* p, size_t n4) {  // constant data
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x)
+        asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + i), "f"(1.f), "f"(1.f), "f"(1.f), "f"(1.f) : "memory");
+}
+// each warp writes a contiguous 64 KB run with 16-B stores (512 B per instruction)
+__global__ void v4run(float4* p, size_t n4) {
+    const size_t w = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
+    const size_t nw = (size_t(gridDim.x) * blockDim.x) >> 5;
+    const int l = threadIdx.x & 31;
+    const size_t run = 4096;  // float4 per run = 64 KB
+    for (size_t r = w; r * run < n4; r += nw)
+        for (size_t i = l; i < run; i += 32) {
+            const size_t k = r * run + i;
+            asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + k), "f"(float(k)), "f"(float(k + 1)), "f"(float(k + 2)), "f"(float(k + 3)) : "memory");
+        }
+}
 __global__ void s1(float* p, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p + i), "f"(float(i)) : "memory");
@@ -46,7 +62,7 @@ int main() {
     float* p; cudaMalloc(&p, bytes);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaFuncSetAttribute(tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2 * 8192);
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 6; ++mode) {
         float best = 1e9;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(a);
@@ -54,12 +70,14 @@ int main() {
             if (mode == 1) v4<<<sms * 8, 256>>>(reinterpret_cast<float4*>(p), n / 4);
             if (mode == 2) s1<<<sms * 8, 256>>>(p, n);
             if (mode == 3) tma<<<sms * 2, 256, 8 * 2 * 8192>>>(p, n);
+            if (mode == 4) v4c<<<sms * 8, 256>>>(reinterpret_cast<float4*>(p), n / 4);
+            if (mode == 5) v4run<<<sms * 8, 256>>>(reinterpret_cast<float4*>(p), n / 4);
             cudaEventRecord(b); cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
             if (ms < best) best = ms;
         }
         printf("mode %d (%s): best %.3f ms = %.1f GB/s  [%s]\n", mode,
-               mode == 0 ? "memset" : mode == 1 ? "st.cs v4" : mode == 2 ? "st.cs 4B" : "tma bulk",
+               mode == 0 ? "memset" : mode == 1 ? "st.cs v4" : mode == 2 ? "st.cs 4B" : mode == 3 ? "tma bulk" : mode == 4 ? "st.cs v4 const" : "st.cs v4 64KB runs",
                best, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
