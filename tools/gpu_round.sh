@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -q -rs > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo bench_ref=$?
-for c in c2 c3 c4 c5; do
+for c in c2 c3 c4 c5 lang; do
   timeout 300 python tools/profile_case.py $c > gpurun_out/plain_$c.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$c.csv python tools/profile_case.py $c > gpurun_out/ncu_l_$c.log 2>&1; echo launches_$c=$?
 done
@@ -15,3 +15,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gen_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bulk -s 2 -c 1 -o gpurun_out/full_bulk python tools/profile_case.py c3 > gpurun_out/ncu_f_c3.log 2>&1; echo full_c3=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:consume -s 2 -c 1 -o gpurun_out/full_consume python tools/profile_case.py c4 > gpurun_out/ncu_f_c4.log 2>&1; echo full_c4=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gaussian -s 2 -c 1 -o gpurun_out/full_gaussian python tools/profile_case.py c5 > gpurun_out/ncu_f_c5.log 2>&1; echo full_c5=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:langevin -s 2 -c 1 -o gpurun_out/full_langevin python tools/profile_case.py lang > gpurun_out/ncu_f_lang.log 2>&1; echo full_lang=$?

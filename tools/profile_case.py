@@ -1,6 +1,6 @@
 """Small, ncu-friendly drivers for one BASELINE config each (1 GPU).
 
-    python tools/profile_case.py c2|c3|c4|c5|jump [--warmup W]
+    python tools/profile_case.py c2|c3|c4|c5|lang|jump [--warmup W]
 
 Runs W warm-up repetitions and one more of the config's GPU job, so an ncu
 capture with `-k regex:<kernel> -s W -c 1` lands on a warm launch.
@@ -19,7 +19,7 @@ import paper_2512_00093_b200 as rb  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["c2", "c3", "c4", "c5", "jump"])
+    ap.add_argument("case", choices=["c2", "c3", "c4", "c5", "lang", "jump"])
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--c4-streams", type=int, default=1 << 16)
     args = ap.parse_args()
@@ -49,6 +49,17 @@ def main():
         st = rb.make_streams(42, 2**64, n)
         for _ in range(reps):
             rb.consume(st, 1 << 20)
+    elif args.case == "lang":
+        # fix-langevin-style consumer, one launch per MD step, 2^24 atoms (config 5 streams)
+        n = 1 << 24
+        g = rb.gauss_states_from(rb.make_streams(7, 2**50, n))
+        v = torch.randn((n, 3), dtype=torch.float64, device="cuda")
+        f = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+        ty = torch.ones(n, dtype=torch.int32, device="cuda")
+        g1, g2 = rb.langevin_factors([0.0, 1.0], 0.1, 0.005)
+        d1, d2 = torch.from_numpy(g1).cuda(), torch.from_numpy(g2).cuda()
+        for _ in range(reps):
+            rb.langevin(g, v, f, ty, d1, d2, 1.0, rb.NOISE_UNIFORM)
     else:
         n = 1 << 20
         st = rb.make_streams(7, 2**50, n)
