@@ -10,13 +10,17 @@
 // back to ring position (i0 - s) mod 97, so the state is written back exactly
 // as per_stream calls of step() leave it. No shuffles, no shared-memory
 // traffic for generation: per output one IADD for the lag recurrence, two for
-// v (VIADD + VIADDMNMX), two for the output, one for the sum, and the
-// histogram update.
+// v (VIADD + VIADDMNMX), two for the output, half an IADD3 for the sum, and
+// five for the histogram (shift, IMAD address, LOP3 + VIMNMX increment, ATOMS.ADD).
 //
-// Histogram: thread-private u16 counters in shared memory, thread t owning
-// bank t mod 32 (word (bin >> 1) * kCT + t, half bin & 1): conflict-free and
-// atomic-free. A thread flushes them into its stream's u32 histogram in HBM at
-// least every 65,535 outputs, so a u16 never overflows.
+// Histogram: thread-private counters in shared memory, thread t owning bank
+// t mod 32: the 32-bit word (bin >> 1) * kCT + t holds bin 2w in its low half
+// and bin 2w + 1 in its high half. One output is ONE shared-memory reduction
+// (red.shared.add, conflict-free since every lane hits its own bank) adding
+// inc = max(u & 2^16, 1), i.e. 1 or 2^16 (measured 4 % faster than the
+// equivalent (u & 2^16) | 1 with a subtraction at flush time). A thread
+// flushes its counters into its stream's u32 histogram in HBM at least every
+// 65,475 outputs, so the low half never carries into the high one.
 #include <cstdint>
 
 #include "ranmar_device.cuh"
@@ -26,7 +30,7 @@ namespace rb {
 namespace {
 
 constexpr int kCT = 384;                               // threads (streams) per block
-constexpr int kRows = 128;                             // u16 pairs per thread
+constexpr int kRows = 128;                             // counter words per thread
 constexpr size_t kConsumeSmem = size_t(kRows) * kCT * 4;  // 192 KB
 constexpr int kBodiesPerFlush = 65535 / 97;            // 675 bodies = 65,475 outputs
 
@@ -35,33 +39,14 @@ __device__ __forceinline__ int mod97c(int64_t x) {
     return static_cast<int>(r < 0 ? r + 97 : r);
 }
 
-// Byte address of bin u >> 16 in this thread's column, (bin >> 1) 4 kCT + (bin & 1) 2,
-// written as bin 2 kCT + (bin & 1) kHalfFix with kHalfFix = 2 - 2 kCT: SHF, LOP3 and
-// two IMADs (the second multiplier comes in as a kernel argument so ptxas keeps
-// the IMAD instead of turning it into a compare and two selects).
-__device__ __forceinline__ uint32_t hist_addr(uint32_t hb, uint32_t u, uint32_t half_fix) {
-    const uint32_t bin = u >> 16;
-    const uint32_t a = hb + bin * (2 * kCT);
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(bin & 1u), "r"(half_fix), "r"(a));
-    return r;
-}
-
-__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u, uint32_t hf) {
-    const uint32_t a = hist_addr(hb, u, hf);
-    uint32_t c;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(a));
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(c + 1) : "memory");
-}
-
-// Adds (or stores, first time) this thread's u16 counters into gh[256] and
+// Adds (or stores, first time) this thread's counters into gh[256] and
 // optionally zeroes them.
 __device__ __forceinline__ void flush(uint32_t* col, uint32_t* __restrict__ gh, bool accumulate,
                                       bool zero) {
 #pragma unroll 4
     for (int w = 0; w < kRows; ++w) {
         const uint32_t x = col[w * kCT];
-        const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
+        const uint32_t hi = x >> 16, lo = x & 0xFFFFu;
         if (accumulate) {
             gh[2 * w] += lo;
             gh[2 * w + 1] += hi;
@@ -73,25 +58,17 @@ __device__ __forceinline__ void flush(uint32_t* col, uint32_t* __restrict__ gh, 
     }
 }
 
-// Two outputs' updates with both loads issued before either store, so the
-// load -> add -> store latency is paid once per pair. If both land in the
-// same counter, both loads saw the same value and the second store (v + 2)
-// overwrites the first (v + 1).
-__device__ __forceinline__ void hist_add2(uint32_t hb, uint32_t u1, uint32_t u2, uint32_t hf) {
-    const uint32_t a1 = hist_addr(hb, u1, hf);
-    const uint32_t a2 = hist_addr(hb, u2, hf);
-    uint32_t c1, c2;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c1) : "r"(a1));
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c2) : "r"(a2));
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "r"(c1 + 1) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a2), "r"(c2 + 1 + (a1 == a2 ? 1u : 0u)) : "memory");
+// One output's histogram update: a single shared-memory reduction.
+__device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u) {
+    const uint32_t a = hb + (u >> 17) * (4 * kCT);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(max(u & 0x10000u, 1u)) : "memory");
 }
 
 template <int S>
 struct Body {
     // steps at compile-time slots S and S + 1, then the rest of the body
     static __device__ __forceinline__ void run(uint32_t (&X)[97], uint32_t& V, uint32_t& s32,
-                                               uint32_t hb, uint32_t hf) {
+                                               uint32_t hb) {
         X[S] -= X[(S + 64) % 97];
         V = add_mod_m(V, kStepA);
         const uint32_t u1 = (X[S] - V) & kMask;
@@ -99,26 +76,26 @@ struct Body {
         V = add_mod_m(V, kStepA);
         const uint32_t u2 = (X[S + 1] - V) & kMask;
         s32 += u1 + u2;
-        hist_add2(hb, u1, u2, hf);
-        Body<S + 2>::run(X, V, s32, hb, hf);
+        hist_add(hb, u1);
+        hist_add(hb, u2);
+        Body<S + 2>::run(X, V, s32, hb);
     }
 };
 template <>
 struct Body<96> {  // the 97th step alone
     static __device__ __forceinline__ void run(uint32_t (&X)[97], uint32_t& V, uint32_t& s32,
-                                               uint32_t hb, uint32_t hf) {
+                                               uint32_t hb) {
         X[96] -= X[63];
         V = add_mod_m(V, kStepA);
         const uint32_t u = (X[96] - V) & kMask;
         s32 += u;
-        hist_add(hb, u, hf);
+        hist_add(hb, u);
     }
 };
 
 __global__ void __launch_bounds__(kCT, 1)
     consume_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
-                   uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status,
-                   uint32_t half_fix) {
+                   uint64_t* __restrict__ sums, uint32_t* __restrict__ hist, uint32_t* status) {
     extern __shared__ uint32_t hsm[];  // [kRows][kCT]
     const int t = threadIdx.x;
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kCT + t;
@@ -149,7 +126,7 @@ __global__ void __launch_bounds__(kCT, 1)
     int since = 0;
     for (uint64_t b = 0; b < bodies; ++b) {
         uint32_t s32 = 0;  // 97 x (2^24 - 1) < 2^31
-        Body<0>::run(X, V, s32, hb, half_fix);
+        Body<0>::run(X, V, s32, hb);
         sum64 += s32;
         if (++since == kBodiesPerFlush) {
             flush(col, gh, flushed, true);
@@ -166,7 +143,7 @@ __global__ void __launch_bounds__(kCT, 1)
         V = add_mod_m(V, kStepA);
         const uint32_t u = (L[s] - V) & kMask;
         sum64 += u;
-        hist_add(hb, u, half_fix);
+        hist_add(hb, u);
     }
     // slot s <-> ring position (i0 - s) mod 97, whatever N is
 #pragma unroll
@@ -194,7 +171,7 @@ cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t 
     const uint64_t blocks = (n_streams + kCT - 1) / kCT;
     count_launch();
     consume_kernel<<<static_cast<unsigned>(blocks), kCT, kConsumeSmem, stream>>>(
-        d_states, n_streams, per_stream, d_sums, d_hist, status, static_cast<uint32_t>(2 - 2 * kCT));
+        d_states, n_streams, per_stream, d_sums, d_hist, status);
     return cudaGetLastError();
 }
 
