@@ -461,12 +461,14 @@ __global__ void put_state_kernel(ranmar_state s, ranmar_state* dst) {
 //    the canonical vector, reversed by decanonicalize), lane rg owns rows
 //    4rg .. 4rg + 3: a 4 x 8 register tile, one LDS.128 of T and one sliding
 //    LDS of the extension per j for 32 IMADs;
-//  * warps 0-3 add column m = 0 (state word 96) for one row per lane and
-//    write the record tail (lane[96], i, j, v) as one 16-B store;
+//  * column m = 0 (state word 96) is spread over all warps: thread t sums a
+//    third of row (t & 127)'s terms into a shared-memory accumulator
+//    (red.shared.add, double-buffered per anchor), and after the next barrier
+//    128 threads write the record tails (lane[96], i, j, v) as 16-B stores;
 //  * results go straight from registers to HBM as 16-B stores (no staging).
 constexpr int kBulkWarps = 12;
 constexpr int kBulkThreads = 32 * kBulkWarps;
-constexpr size_t kBulkSmem = (size_t(kPolyN) * kRows + 2 * kWAnchor) * 4;
+constexpr size_t kBulkSmem = (size_t(kPolyN) * kRows + 2 * kWAnchor + 2 * kRows) * 4;
 
 struct BulkArgs {
     const uint32_t* W1;   // anchors' extensions, H x kWAnchor
@@ -479,10 +481,26 @@ struct BulkArgs {
     ranmar_state base;    // stream 0 verbatim (when first == 0)
 };
 
+// Record tail of row `row` of anchor h: word 96 (column 0, summed in C0), the
+// normalised cursors and v (closed form, jump_arith with k J mod m); zeroes the
+// row's accumulator for the anchor after next.
+__device__ __forceinline__ void bulk_tail(const BulkArgs& args, uint32_t* C0, uint64_t h, int row) {
+    const uint32_t a0 = C0[row];
+    C0[row] = 0;
+    const uint64_t row0 = h * kRows;
+    const uint64_t rows = args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows;
+    if (static_cast<uint64_t>(row) >= rows || (args.first == 0 && h == 0 && row == 0)) return;
+    const uint64_t k = args.first + row0 + row;
+    const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
+    const uint32_t v = static_cast<uint32_t>((args.v_base + (kMod - dec)) % kMod);
+    *reinterpret_cast<uint4*>(args.out[row0 + row].lane + 96) = make_uint4(a0 & kMask, 96u, 32u, v);
+}
+
 __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_constant__ BulkArgs args) {
     extern __shared__ uint4 sm4[];
     uint32_t* Tt = reinterpret_cast<uint32_t*>(sm4);  // [97][128]
     uint32_t* Wb = Tt + kPolyN * kRows;               // [2][196]
+    uint32_t* C0 = Wb + 2 * kWAnchor;                 // [2][128] column-0 sums
     const int t = threadIdx.x;
     const int g = t >> 5, rg = t & 31;
     const int m0 = 89 - 8 * g;
@@ -493,10 +511,24 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
     }
     uint64_t h = blockIdx.x;
     if (h < args.H && t < 193) Wb[t] = args.W1[h * kWAnchor + t];
+    if (t < 2 * kRows) C0[t] = 0;
     __syncthreads();
 
+    const int crow = t & (kRows - 1), cpart = t >> 7;  // column 0: row, third of the terms
+    const int cj0 = 33 * cpart, cj1 = cpart == 2 ? kPolyN : cj0 + 33;
+    uint64_t hprev = ~0ull;
     for (int it = 0; h < args.H; ++it, h += gridDim.x) {
         const uint32_t* W = Wb + (it & 1) * kWAnchor;
+        if (hprev != ~0ull && t < kRows) bulk_tail(args, C0 + ((it & 1) ^ 1) * kRows, hprev, t);
+        {   // column 0 partial sums (the buffer was zeroed before the last barrier)
+            uint32_t a0 = 0;
+#pragma unroll 11
+            for (int j = cj0; j < cj1; ++j) a0 += Tt[j * kRows + crow] * W[j];
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(static_cast<uint32_t>(
+                             __cvta_generic_to_shared(C0 + (it & 1) * kRows + crow))),
+                         "r"(a0)
+                         : "memory");
+        }
         const uint64_t hn = h + gridDim.x;
         if (hn < args.H && t < 193) Wb[((it + 1) & 1) * kWAnchor + t] = args.W1[hn * kWAnchor + t];
 
@@ -544,22 +576,14 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
             dst[1] = make_uint4(acc[rr][3] & kMask, acc[rr][2] & kMask, acc[rr][1] & kMask,
                                 acc[rr][0] & kMask);
         }
-        if (g < 4) {  // column m = 0 -> state word 96, plus i, j, v
-            const int row = 32 * g + rg;
-            uint32_t a0 = 0;
-#pragma unroll 8
-            for (int j = 0; j < kPolyN; ++j) a0 += Tt[j * kRows + row] * W[j];
-            if (static_cast<uint64_t>(row) < rows && !(skip0 && row == 0)) {
-                const uint64_t k = args.first + row0 + row;
-                const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
-                const uint32_t v = static_cast<uint32_t>((args.v_base + (kMod - dec)) % kMod);
-                *reinterpret_cast<uint4*>(args.out[row0 + row].lane + 96) =
-                    make_uint4(a0 & kMask, 96u, 32u, v);
-            }
-        }
         if (skip0 && t < 100)
             reinterpret_cast<uint32_t*>(args.out)[t] = reinterpret_cast<const uint32_t*>(&args.base)[t];
+        hprev = h;
         __syncthreads();
+    }
+    if (hprev != ~0ull && t < kRows) {
+        const int it_last = static_cast<int>((hprev - blockIdx.x) / gridDim.x);
+        bulk_tail(args, C0 + (it_last & 1) * kRows, hprev, t);
     }
 }
 
