@@ -161,13 +161,8 @@ cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t 
                            uint64_t* d_sums, uint32_t* d_hist, uint32_t* status,
                            cudaStream_t stream) {
     if (n_streams == 0) return cudaSuccess;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(consume_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kConsumeSmem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = ensure_smem(consume_kernel, static_cast<int>(kConsumeSmem), configured)) return e;
     const uint64_t blocks = (n_streams + kCT - 1) / kCT;
     count_launch();
     consume_kernel<<<static_cast<unsigned>(blocks), kCT, kConsumeSmem, stream>>>(

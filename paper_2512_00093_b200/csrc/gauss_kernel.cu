@@ -231,13 +231,8 @@ cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_
                               uint64_t steps, double* d_out, uint32_t* status,
                               cudaStream_t stream) {
     const int smem = 97 * kGT * 4;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gaussian_kernel<K>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = ensure_smem(gaussian_kernel<K>, smem, configured)) return e;
     const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
     count_launch();
     gaussian_kernel<K><<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(

@@ -653,13 +653,8 @@ cudaError_t launch_put_state(const ranmar_state& s, ranmar_state* dst, cudaStrea
 cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
                         uint64_t first, uint64_t n, uint32_t v_base, uint32_t jm,
                         const ranmar_state& base, int sm_count, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kBulkSmem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), configured)) return e;
     BulkArgs a{W1, H, Tt, out, first, n, v_base, jm, base};
     const uint64_t grid = H < uint64_t(2 * sm_count) ? H : uint64_t(2 * sm_count);
     count_launch();

@@ -15,6 +15,7 @@
 //    (canonicalize, jump.hpp:32-37, with u[k] = x_{k-97}).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 
 #include "ranmar_b200.h"
@@ -31,6 +32,19 @@ constexpr uint32_t kStepA = kMod - kDelta;        // per-step increment of v (co
 
 // Launch counter behind ranmar_kernel_launches() (incremented by every launcher).
 void count_launch(int n = 1);
+
+// Raises a kernel's dynamic shared-memory limit once per device: the attribute
+// belongs to the device context, and one process may drive several devices.
+template <class Kernel>
+inline cudaError_t ensure_smem(Kernel* kernel, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+    if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_relaxed);
+    return e;
+}
 
 // Status bits OR-ed into the library's device status word.
 constexpr uint32_t kStatusBadState = 1u;          // cursor separation / range violated
