@@ -53,3 +53,9 @@ $(CLI): tools/ranmar_cli.cpp include/ranmar_b200.hpp $(LIB)
 	@mkdir -p $(dir $(CLI))
 	g++ -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -L$(PKG)/lib -lranmar_b200 \
 	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../lib' -Wl,-rpath,/usr/local/cuda/lib64 -o $@
+
+# Microbenchmarks behind profiles/r1_micro.txt (run on a GPU box)
+MICRO := tools/micro/wbw tools/micro/ce tools/micro/pipes tools/micro/dtile
+micro: $(MICRO)
+tools/micro/%: tools/micro/%.cu
+	$(NVCC) -gencode arch=compute_100a,code=sm_100a -O3 -o $@ $<
