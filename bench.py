@@ -338,17 +338,22 @@ def run_ours(args, rank, world, local):
     # ---- e2e: the same job through the host-buffer C-ABI path ----
     e2e = None
     if not args.no_e2e:
+        # Pinned host output per rank: the full 16 GiB unless the ranks together would
+        # pin more than a quarter of the host's RAM (then the leading streams of the range).
+        import psutil
+        budget = psutil.virtual_memory().total // 4 // world
+        n_e2e = int(min(n, max(1, budget // (per * 4))))
         ctx = rb.Context(local)
-        host_states = np.zeros(n, rb.STATE_DTYPE)
-        host_out = torch.empty(n * per, dtype=torch.float32, pin_memory=True).numpy()
+        host_states = np.zeros(n_e2e, rb.STATE_DTYPE)
+        host_out = torch.empty(n_e2e * per, dtype=torch.float32, pin_memory=True).numpy()
         e2e_steps = max(1, min(args.steps, 3))
-        ctx.make_streams(C2["seed"], C2["j"], n, first=first, out=host_states)
+        ctx.make_streams(C2["seed"], C2["j"], n_e2e, first=first, out=host_states)
         ctx.generate(host_states, per, "f32", out=host_out)  # warm-up
         h2d = d2h = 0
         barrier(world)
         tt = time.perf_counter()
         for _ in range(e2e_steps):
-            ctx.make_streams(C2["seed"], C2["j"], n, first=first, out=host_states)
+            ctx.make_streams(C2["seed"], C2["j"], n_e2e, first=first, out=host_states)
             a, b = ctx.traffic()
             ctx.generate(host_states, per, "f32", out=host_out)
             c, d = ctx.traffic()
@@ -356,8 +361,9 @@ def run_ours(args, rank, world, local):
         e2e_s = max_over_ranks((time.perf_counter() - tt) / e2e_steps, world)
         # host result equals the device result of the timed step
         assert np.array_equal(host_out[:per * 4], out[:per * 4].cpu().numpy())
-        e2e = {"value": uniforms_step / e2e_s, "unit": "uniforms/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+        e2e = {"value": n_e2e * per * world / e2e_s, "unit": "uniforms/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+               "streams_per_rank": n_e2e,
                "path": "ranmar_ctx_make_streams + ranmar_ctx_generate_f32 into pinned host memory"}
         del host_out
         ctx.close()
