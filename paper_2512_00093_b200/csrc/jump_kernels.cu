@@ -19,10 +19,11 @@
 //                         cached squares), one CTA per exponent, warps reduce
 //                         strided factor subsets then a tree.
 //  tables_kernel          offset tables Tab_L[r] = P_{r 128^L J}, r < 128.
-//  apply_kernel      K3b  u * P(A) for a batch of states as a Hankel product
+//  apply2_kernel     K3b  u * P(A) for a batch of states as a Hankel product
 //                         out[m] = sum_j p_j w[j + m] over the recurrence
 //                         extension w of u (no sequential Horner chain), + K3c
-//                         the closed-form arithmetic jump.
+//                         the closed-form arithmetic jump; 64 states per CTA,
+//                         2 x 8 register tiles per lane.
 //  level_kernel      K3b  one level of the base-128 stream-start tree
 //                         S_L[k] = apply(S_{L+1}[k / 128], Tab_L[k % 128]).
 //  bulk_kernel       K3b  level 0 (all stream starts): per anchor a 128 x 97
@@ -294,68 +295,118 @@ __device__ __forceinline__ void extend_items(uint32_t* W, int stride, int items,
     }
 }
 
-// ---- K3b/K3c for a batch: out[k] = jump(in[k]) with one shared P and dec.
-// (ranmar_jump_dev and the first anchor of make_streams.)
+// Level kernels process kApplyItems states per CTA (shared-memory Hankel tiles).
 constexpr int kApplyItems = 8;
-constexpr int kApplyThreads = kApplyItems * 13;  // 104: (item, column group of 8)
-constexpr int kWExt = 208;
-constexpr int kWStride = kWExt + 1;               // odd stride spreads banks
 constexpr int kJPad = 104;                        // coefficients padded to 13 x 8
 
-__global__ void __launch_bounds__(kApplyThreads)
-    apply_kernel(const ranmar_state* in, ranmar_state* out, uint64_t n,
-                 const uint32_t* __restrict__ P, uint32_t dec) {
-    __shared__ uint32_t W[kApplyItems * kWStride];
-    __shared__ uint32_t p[kJPad];
-    __shared__ uint32_t vin[kApplyItems];
-    __shared__ int iin[kApplyItems];
-    const int t = threadIdx.x;
-    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kApplyItems;
-    const int items = static_cast<int>(n - k0 < (uint64_t)kApplyItems ? n - k0 : (uint64_t)kApplyItems);
-    for (int k = t; k < kJPad; k += kApplyThreads) p[k] = k < kPolyN ? P[k] : 0u;
-    if (t < items) {
-        iin[t] = in[k0 + t].i;
-        vin[t] = in[k0 + t].v;
-    }
-    __syncthreads();
-    for (int x = t; x < items * kPolyN; x += kApplyThreads) {
-        const int it = x / kPolyN, kk = x - it * kPolyN;
-        W[it * kWStride + kk] = in[k0 + it].lane[(iin[it] - kk + 97) % 97];
-    }
-    __syncthreads();
-    extend_items(W, kWStride, items, kWExt, t, kApplyThreads);
+// ---- K3b/K3c for a batch, tiled: out[k] = jump(in[k]) with one shared P.
+// 64 states per CTA (3 CTAs per SM; 128 per CTA measured 16 % slower: its
+// gather phase overlaps less): canonical vectors in shared memory (odd stride 193),
+// extended by the recurrence to 193 terms, then the Hankel products
+// out[m] = sum_j p_j w[j + m] as register tiles: warp g owns columns
+// m0 = 89 - 8g .. 96 - 8g (state words 8g .. 8g + 7, 16-B stores), lane l owns
+// states l and l + 32 with an 8-wide sliding window each: per j one broadcast
+// LDS of p_j, two LDS of the windows and 16 IMADs. Column 0 (word 96) is
+// summed by all threads in sixths with shared-memory atomics.
+constexpr int kA2Items = 64;
+constexpr int kA2Rows = kA2Items / 32;  // states per lane
+constexpr int kA2Threads = 384;
+constexpr int kA2Stride = 193;  // odd: lanes l (+32 rr) hit distinct banks
+constexpr size_t kA2Smem = (size_t(kA2Items) * kA2Stride + 128 + 2 * kA2Items) * 4;
 
-    const int it = t / 13, cg = t - it * 13;
-    if (it < items) {
-        const uint32_t* w_it = W + it * kWStride + 8 * cg;
-        uint32_t acc[8], win[8];
+__global__ void __launch_bounds__(kA2Threads, 3)
+    apply2_kernel(const ranmar_state* in, ranmar_state* out, uint64_t n,
+                  const uint32_t* __restrict__ P, uint32_t dec) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* W = sm;                                   // [128][193]
+    uint32_t* p = W + kA2Items * kA2Stride;             // [128] (97 used)
+    uint32_t* C0 = p + 128;                             // [kA2Items] column-0 sums
+    uint32_t* vin = C0 + kA2Items;                      // [128]
+    const int t = threadIdx.x;
+    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kA2Items;
+    const int items = static_cast<int>(n - k0 < (uint64_t)kA2Items ? n - k0 : (uint64_t)kA2Items);
+    if (t < 128) p[t] = t < kPolyN ? P[t] : 0u;
+    if (t < kA2Items) {
+        C0[t] = 0;
+        if (t < items) vin[t] = in[k0 + t].v;
+    }
+    {   // canonical vectors (jump.hpp:32-37): W[it][kk] = lane[(i - kk) mod 97], a warp per state
+        const int g = t >> 5, l = t & 31;
+#pragma unroll 2
+        for (int it = g; it < items; it += kA2Threads / 32) {
+            const ranmar_state* src = in + k0 + it;
+            const int i0 = src->i;
+            uint32_t* Wi = W + it * kA2Stride;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            acc[c] = 0;
-            win[c] = w_it[c];
-        }
-#pragma unroll 1
-        for (int j0 = 0; j0 < kJPad; j0 += 8) {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const uint32_t pj = p[j0 + jj];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) acc[c] += pj * win[(jj + c) & 7];
-                win[jj] = w_it[j0 + jj + 8];
+            for (int kk = l; kk < kPolyN; kk += 32) {
+                int q = i0 - kk;
+                q += q < 0 ? 97 : 0;
+                Wi[kk] = src->lane[q];
             }
         }
-        ranmar_state* o = out + k0 + it;
+    }
+    __syncthreads();
+    for (int lo = 97; lo < 193; lo += 33) {  // x_n = x_{n-97} - x_{n-33}, 33 terms at a time
+        const int cnt = 193 - lo < 33 ? 193 - lo : 33;
+        for (int x = t; x < items * cnt; x += kA2Threads) {
+            const int it = x / cnt, nn = lo + (x - it * cnt);
+            uint32_t* Wi = W + it * kA2Stride;
+            Wi[nn] = Wi[nn - 97] - Wi[nn - 33];
+        }
+        __syncthreads();
+    }
+    {   // column 0: state t % 64, a sixth of its terms
+        const int it = t % kA2Items, part = t / kA2Items;
+        const int j0 = 17 * part, j1 = part == 5 ? kPolyN : j0 + 17;
+        const uint32_t* Wi = W + it * kA2Stride;
+        uint32_t a0 = 0;
+#pragma unroll 6
+        for (int j = j0; j < j1; ++j) a0 += p[j] * Wi[j];
+        atomicAdd(C0 + it, a0);
+    }
+    const int g = t >> 5, l = t & 31;
+    const int m0 = 89 - 8 * g;
+    uint32_t acc[kA2Rows][8], win[kA2Rows][8];
+#pragma unroll
+    for (int rr = 0; rr < kA2Rows; ++rr)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const int m = 8 * cg + c;
-            if (m < kPolyN) o->lane[96 - m] = acc[c] & kMask;
+            acc[rr][c] = 0;
+            win[rr][c] = W[(l + 32 * rr) * kA2Stride + m0 + c];
         }
-        if (cg == 0) {
-            o->i = 96;  // decanonicalize, jump.hpp:42-48
-            o->j = 32;
-            const uint32_t v = vin[it];
-            o->v = static_cast<uint32_t>((static_cast<uint64_t>(v) + (kMod - dec)) % kMod);
+#pragma unroll 1
+    for (int j0 = 0; j0 < 96; j0 += 8) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const uint32_t pj = p[j0 + jj];
+#pragma unroll
+            for (int rr = 0; rr < kA2Rows; ++rr)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[rr][c] += pj * win[rr][(jj + c) & 7];
+#pragma unroll
+            for (int rr = 0; rr < kA2Rows; ++rr) win[rr][jj] = W[(l + 32 * rr) * kA2Stride + m0 + j0 + jj + 8];
         }
+    }
+    {   // j = 96: slot c holds W[96 + m0 + c]
+        const uint32_t pj = p[96];
+#pragma unroll
+        for (int rr = 0; rr < kA2Rows; ++rr)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[rr][c] += pj * win[rr][c];
+    }
+#pragma unroll
+    for (int rr = 0; rr < kA2Rows; ++rr) {
+        const int it = l + 32 * rr;
+        if (it >= items) continue;
+        uint4* dst = reinterpret_cast<uint4*>(out[k0 + it].lane + 8 * g);
+        // word 8g + q holds canonical column 96 - 8g - q = m0 + 7 - q (decanonicalize, jump.hpp:42-48)
+        dst[0] = make_uint4(acc[rr][7] & kMask, acc[rr][6] & kMask, acc[rr][5] & kMask, acc[rr][4] & kMask);
+        dst[1] = make_uint4(acc[rr][3] & kMask, acc[rr][2] & kMask, acc[rr][1] & kMask, acc[rr][0] & kMask);
+    }
+    __syncthreads();
+    if (t < items) {  // word 96, cursors i = 96, j = 32, and v by jump_arith
+        const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(vin[t]) + (kMod - dec)) % kMod);
+        *reinterpret_cast<uint4*>(out[k0 + t].lane + 96) = make_uint4(C0[t] & kMask, 96u, 32u, v);
     }
 }
 
@@ -624,9 +675,11 @@ cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t
 cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, const uint32_t* P,
                          uint32_t dec, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
-    const uint64_t blocks = (n + kApplyItems - 1) / kApplyItems;
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), configured)) return e;
     count_launch();
-    apply_kernel<<<static_cast<unsigned>(blocks), kApplyThreads, 0, stream>>>(in, out, n, P, dec);
+    apply2_kernel<<<static_cast<unsigned>((n + kA2Items - 1) / kA2Items), kA2Threads, kA2Smem,
+                    stream>>>(in, out, n, P, dec);
     return cudaGetLastError();
 }
 
