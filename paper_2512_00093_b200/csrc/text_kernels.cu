@@ -17,22 +17,32 @@ namespace rb {
 
 namespace {
 
+// Decimal digits of x: independent compares instead of a division chain.
 __device__ __forceinline__ int ndigits(uint32_t x) {
-    int d = 1;
-    while (x >= 10) {
-        x /= 10;
-        ++d;
-    }
-    return d;
+    return 1 + (x >= 10u) + (x >= 100u) + (x >= 1000u) + (x >= 10000u) + (x >= 100000u) +
+           (x >= 1000000u) + (x >= 10000000u) + (x >= 100000000u) + (x >= 1000000000u);
 }
 
+// x in decimal at p (no terminator); returns the end. The low and high 4-digit
+// groups are converted by two independent chains.
 __device__ __forceinline__ char* put_uint(char* p, uint32_t x) {
     const int d = ndigits(x);
-    for (int k = d - 1; k >= 0; --k) {
-        p[k] = static_cast<char>('0' + x % 10);
-        x /= 10;
+    uint32_t hi = x / 10000u, lo = x - hi * 10000u;
+    char* e = p + d;
+    int k = d - 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // the low group (digits d-1 .. d-4)
+        if (k < 0) break;
+        const uint32_t t = lo / 10u;
+        p[k--] = static_cast<char>('0' + (lo - 10u * t));
+        lo = t;
     }
-    return p + d;
+    while (k >= 0) {  // the high group (at most 6 more digits)
+        const uint32_t t = hi / 10u;
+        p[k--] = static_cast<char>('0' + (hi - 10u * t));
+        hi = t;
+    }
+    return e;
 }
 
 // serialize.hpp:21-40 line by line: 0 "ranmar24 v1", 1 "i <i+1> j <j+1>",
@@ -78,14 +88,22 @@ __device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* 
     *p = '\n';
 }
 
+// warp per state (coalesced lane reads): the exact byte length of its text
 __global__ void text_len_kernel(const ranmar_state* __restrict__ st, uint64_t n,
                                 uint64_t* __restrict__ len) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int l = threadIdx.x & 31;
     if (k >= n) return;
     const ranmar_state& s = st[k];
-    uint64_t L = 0;
-    for (int line = 0; line < 100; ++line) L += line_len(s, line);
-    len[k] = L;
+    uint32_t L = 0;
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+        const int line = pass * 32 + l;
+        if (line < 100) L += static_cast<uint32_t>(line_len(s, line));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (l == 0) len[k] = L;
 }
 
 // exclusive scan, 1024 items per block; block totals to bsum
@@ -134,28 +152,56 @@ __global__ void copy_u64_kernel(uint64_t* __restrict__ dst, const uint64_t* __re
     *dst = *src;
 }
 
-// warp per state: lane handles lines lane, lane+32, lane+64, lane+96
-__global__ void to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n,
-                               const uint64_t* __restrict__ off, char* __restrict__ text) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int l = threadIdx.x & 31;
-    if (k >= n) return;
-    const ranmar_state& s = st[k];
-    char* base = text + off[k];
-    uint32_t before = 0;  // bytes of the lines of previous passes
+// Upper bound of one state's text: 12 + 10 + 11 + 97 * 14.
+constexpr uint64_t kMaxStateText = 12 + 10 + 11 + 97 * 14;
+constexpr int kTTStates = 8;  // states (warps) per CTA
+constexpr int kTTStage = kTTStates * static_cast<int>(kMaxStateText) + 16;
+
+// Warp per state: lane handles lines lane, lane+32, lane+64, lane+96, the
+// line offsets by a warp prefix sum. The CTA's 8 consecutive texts are
+// formatted into shared memory, placed at the same offset mod 16 as in the
+// output, and then written out as aligned 16-B stores (byte stores only for
+// the unaligned head and tail of the CTA's range).
+__global__ void __launch_bounds__(32 * kTTStates)
+    to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n,
+                   const uint64_t* __restrict__ off, char* __restrict__ text) {
+    __shared__ __align__(16) char stage[kTTStage];
+    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kTTStates;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint64_t k = k0 + w;
+    const uint64_t kend = k0 + kTTStates < n ? k0 + kTTStates : n;
+    const uint64_t g0 = off[k0], g1 = off[kend];
+    const uint32_t shift = static_cast<uint32_t>(g0 & 15);
+    if (k < n) {
+        const ranmar_state& s = st[k];
+        char* base = stage + shift + (off[k] - g0);
+        uint32_t before = 0;  // bytes of the lines of previous passes
 #pragma unroll
-    for (int pass = 0; pass < 4; ++pass) {
-        const int line = pass * 32 + l;
-        const uint32_t len = line < 100 ? static_cast<uint32_t>(line_len(s, line)) : 0u;
-        uint32_t incl = len;
+        for (int pass = 0; pass < 4; ++pass) {
+            const int line = pass * 32 + l;
+            const uint32_t len = line < 100 ? static_cast<uint32_t>(line_len(s, line)) : 0u;
+            uint32_t incl = len;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (l >= o) incl += y;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (l >= o) incl += y;
+            }
+            if (line < 100) put_line(s, line, base + before + incl - len);
+            before += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (line < 100) put_line(s, line, base + before + incl - len);
-        before += __shfl_sync(0xffffffffu, incl, 31);
     }
+    __syncthreads();
+    const uint64_t a = (g0 + 15) & ~uint64_t(15), b = g1 & ~uint64_t(15);
+    const int t = threadIdx.x;
+    if (a >= b) {  // no aligned chunk: bytes only
+        for (uint64_t x = g0 + t; x < g1; x += blockDim.x) text[x] = stage[shift + (x - g0)];
+        return;
+    }
+    if (g0 + t < a) text[g0 + t] = stage[shift + t];
+    if (b + t < g1) text[b + t] = stage[shift + (b - g0) + t];
+    const uint4* src = reinterpret_cast<const uint4*>(stage + shift + (a - g0));
+    uint4* dst = reinterpret_cast<uint4*>(text + a);
+    for (uint64_t q = t; q < (b - a) / 16; q += blockDim.x) dst[q] = src[q];
 }
 
 // ---- parser (serialize.hpp:81-136), thread per state
@@ -237,9 +283,6 @@ __global__ void from_text_kernel(const char* __restrict__ text, const uint64_t* 
 
 }  // namespace
 
-// Upper bound of one state's text: 12 + 10 + 11 + 97 * 14.
-constexpr uint64_t kMaxStateText = 12 + 10 + 11 + 97 * 14;
-
 uint64_t text_bound(uint64_t n) { return n * kMaxStateText; }
 
 constexpr uint64_t kTextChunk = uint64_t(kScanT) * kScanT;  // states per scan (2^20)
@@ -265,8 +308,8 @@ cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_tex
         // the previous chunk wrote off[c0] = its end; keep it as this chunk's base
         uint64_t* base_copy = boff + blocks;
         count_launch(3);
-        text_len_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, stream>>>(d_states + c0,
-                                                                                    m, len);
+        text_len_kernel<<<static_cast<unsigned>((m + 7) / 8), 256, 0, stream>>>(d_states + c0, m,
+                                                                                len);
         if (base) {
             count_launch();
             copy_u64_kernel<<<1, 1, 0, stream>>>(base_copy, base);
@@ -283,8 +326,8 @@ cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_tex
         }
         count_launch();
         total_kernel<<<1, 1, 0, stream>>>(off, m, len);
-        to_text_kernel<<<static_cast<unsigned>((m + 7) / 8), 256, 0, stream>>>(d_states + c0, m,
-                                                                               off, d_text);
+        to_text_kernel<<<static_cast<unsigned>((m + kTTStates - 1) / kTTStates), 32 * kTTStates, 0,
+                         stream>>>(d_states + c0, m, off, d_text);
     }
     return cudaGetLastError();
 }
