@@ -242,16 +242,14 @@ __device__ __forceinline__ bool take_lit(const char*& p, const char* e, const ch
     return true;
 }
 
-__global__ void from_text_kernel(const char* __restrict__ text, const uint64_t* __restrict__ off,
-                                 uint64_t n, ranmar_state* __restrict__ out,
-                                 int32_t* __restrict__ err) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Cursor c{text + off[k], text + off[k + 1]};
+// The reference's strict parser, one thread, on [t0, t1): *out written and
+// *err = 0 on success, else *err = the 1-based line of the first error.
+__device__ void parse_seq(const char* t0, const char* t1, ranmar_state* out, int32_t* err) {
+    Cursor c{t0, t1};
     ranmar_state s;
     int line = 1;
     const char *b, *e;
-    auto fail = [&](int ln) { err[k] = ln; };
+    auto fail = [&](int ln) { *err = ln; };
     if (!next_line(c, b, e) || !(e - b == 11 && take_lit(b, e, "ranmar24 v1", 11))) return fail(line);
     ++line;
     uint64_t i = 0, j = 0, v = 0;
@@ -277,8 +275,156 @@ __global__ void from_text_kernel(const char* __restrict__ text, const uint64_t* 
     }
     for (const char* p = c.p; p < c.end; ++p)
         if (*p != '\n' && *p != '\r' && *p != ' ' && *p != '\t') return fail(line + 1);
-    out[k] = s;
-    err[k] = 0;
+    *out = s;
+    *err = 0;
+}
+
+
+// Warp per state: the text is staged in shared memory with coalesced 16-B
+// loads, the warp finds the line boundaries (32 bytes per step, ordered by a
+// ballot), then lane l checks lines l + 1, l + 33,
+// l + 65 and l + 97 with the same rules as parse_seq, and the first failing
+// line is the warp minimum. Texts longer than the staging buffer (never a
+// valid state with ordinary trailing whitespace) go to parse_seq.
+constexpr int kFTWarps = 4;
+constexpr int kFTCap = 2048;   // staged bytes per warp
+constexpr int kFTLines = 128;  // newline positions kept per warp
+
+__device__ __forceinline__ bool is_digit(char ch) { return ch >= '0' && ch <= '9'; }
+
+// decimal at [p, e): value (fails above 2^32 - 1 or with no digit), advances p
+__device__ __forceinline__ bool num_at(const char* sm, int& p, int e, uint64_t& v) {
+    v = 0;
+    int nd = 0;
+    while (p < e && is_digit(sm[p])) {
+        v = v * 10 + static_cast<uint64_t>(sm[p] - '0');
+        if (v > 0xFFFFFFFFull) return false;
+        ++p;
+        ++nd;
+    }
+    return nd > 0;
+}
+
+__global__ void __launch_bounds__(32 * kFTWarps)
+    from_text_warp_kernel(const char* __restrict__ text, const uint64_t* __restrict__ off,
+                          uint64_t n, ranmar_state* __restrict__ out, int32_t* __restrict__ err) {
+    __shared__ __align__(16) char stage[kFTWarps][kFTCap + 16];
+    __shared__ int nl[kFTWarps][kFTLines];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kFTWarps + w;
+    if (k >= n) return;
+    const uint64_t b = off[k], e = off[k + 1];
+    const int L = static_cast<int>(e - b < uint64_t(1) << 30 ? e - b : uint64_t(1) << 30);
+    if (L > kFTCap) {
+        if (l == 0) parse_seq(text + b, text + e, out + k, err + k);
+        return;
+    }
+    char* sm = stage[w];
+    {   // aligned 16-B chunks covering [b, e); byte shift = b & 15
+        const uint64_t a0 = b & ~uint64_t(15);
+        const int sh = static_cast<int>(b - a0);
+        const int chunks = (sh + L + 15) >> 4;
+        const uint4* src = reinterpret_cast<const uint4*>(text + a0);
+        for (int q = l; q < chunks; q += 32) reinterpret_cast<uint4*>(sm)[q] = src[q];
+        __syncwarp();
+        sm += sh;  // sm[0 .. L) is the text
+    }
+    // newlines, in order: the warp reads 32 consecutive bytes per step (lane l
+    // byte x0 + l, conflict-free) and a ballot places the ones it finds
+    int total_nl = 0;
+    const uint32_t lt = (1u << l) - 1u;
+    for (int x0 = 0; x0 < L && total_nl < kFTLines; x0 += 32) {
+        const bool isnl = x0 + l < L && sm[x0 + l] == '\n';
+        const uint32_t bal = __ballot_sync(0xffffffffu, isnl);
+        const int pos = total_nl + __popc(bal & lt);
+        if (isnl && pos < kFTLines) nl[w][pos] = x0 + l;
+        total_nl += __popc(bal);
+    }
+    __syncwarp();
+    // line ln (1-based) = [start, end) before '\r' stripping; exists iff start < L
+    auto line_span = [&](int ln, int& st, int& en) -> bool {
+        st = ln == 1 ? 0 : nl[w][ln - 2] + 1;
+        if (ln >= 2 && ln - 2 >= total_nl) return false;  // no newline ends line ln - 1
+        if (st >= L) return false;
+        en = ln - 1 < total_nl ? nl[w][ln - 1] : L;
+        if (en > st && sm[en - 1] == '\r') --en;
+        return true;
+    };
+    int bad = 0x7FFFFFFF;  // first failing line seen by this lane
+    uint32_t vals[4] = {0, 0, 0, 0};
+    int32_t si = 0, sj = 0;
+    uint32_t sv = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int ln = l + 1 + 32 * r;
+        if (ln > 100) break;
+        int p, en;
+        bool ok = line_span(ln, p, en);
+        if (ok) {
+            if (ln == 1) {
+                const char h[] = "ranmar24 v1";
+                ok = en - p == 11;
+                for (int c = 0; ok && c < 11; ++c) ok = sm[p + c] == h[c];
+            } else if (ln == 2) {
+                uint64_t i = 0, j = 0;
+                ok = en - p >= 2 && sm[p] == 'i' && sm[p + 1] == ' ';
+                p += 2;
+                ok = ok && num_at(sm, p, en, i);
+                ok = ok && en - p >= 3 && sm[p] == ' ' && sm[p + 1] == 'j' && sm[p + 2] == ' ';
+                p += 3;
+                ok = ok && num_at(sm, p, en, j) && p == en;
+                ok = ok && i >= 1 && i <= 97 && j >= 1 && j <= 97 && (i + 97 - j) % 97 == 64;
+                si = static_cast<int32_t>(i) - 1;
+                sj = static_cast<int32_t>(j) - 1;
+            } else if (ln == 3) {
+                uint64_t v = 0;
+                ok = en - p >= 2 && sm[p] == 'v' && sm[p + 1] == ' ';
+                p += 2;
+                ok = ok && num_at(sm, p, en, v) && p == en && v < kMod;
+                sv = static_cast<uint32_t>(v);
+            } else {
+                uint64_t idx = 0, lane = 0;
+                ok = en - p >= 2 && sm[p] == 'u' && sm[p + 1] == ' ';
+                p += 2;
+                ok = ok && num_at(sm, p, en, idx);
+                ok = ok && p < en && sm[p] == ' ';
+                ++p;
+                ok = ok && num_at(sm, p, en, lane) && p == en &&
+                     idx == static_cast<uint64_t>(ln - 3) && lane <= kMask;
+                vals[r] = static_cast<uint32_t>(lane);
+            }
+        }
+        if (!ok && ln < bad) bad = ln;
+    }
+    // after line 100 only whitespace may follow (serialize.hpp: fail(line + 1))
+    {
+        int tail = L;  // start of what follows line 100
+        if (total_nl >= 100) tail = nl[w][99] + 1;
+        bool ws = true;
+        for (int x = tail + l; x < L; x += 32) {
+            const char ch = sm[x];
+            ws = ws && (ch == '\n' || ch == '\r' || ch == ' ' || ch == '\t');
+        }
+        if (!__all_sync(0xffffffffu, ws) && 101 < bad) bad = 101;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    if (bad != 0x7FFFFFFF) {
+        if (l == 0) err[k] = bad;
+        return;
+    }
+    ranmar_state* o = out + k;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int ln = l + 1 + 32 * r;
+        if (ln >= 4 && ln <= 100) o->lane[ln - 4] = vals[r];
+    }
+    if (l == 1) {
+        o->i = si;
+        o->j = sj;
+    }
+    if (l == 2) o->v = sv;
+    if (l == 0) err[k] = 0;
 }
 
 }  // namespace
@@ -336,8 +482,8 @@ cudaError_t launch_from_text(const char* d_text, const uint64_t* d_off, uint64_t
                              ranmar_state* d_states, int32_t* d_err, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     count_launch();
-    from_text_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(d_text, d_off, n,
-                                                                                 d_states, d_err);
+    from_text_warp_kernel<<<static_cast<unsigned>((n + kFTWarps - 1) / kFTWarps), 32 * kFTWarps, 0,
+                            stream>>>(d_text, d_off, n, d_states, d_err);
     return cudaGetLastError();
 }
 
