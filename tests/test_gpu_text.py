@@ -79,6 +79,13 @@ def test_from_text_errors_match_reference(refvec):
         good.replace("\n", "\r\n"),                    # CRLF is accepted
         good + "\n\n  \t\n",                           # trailing whitespace is accepted
         "",
+        good.rstrip("\n"),                             # no final newline is accepted
+        good + " " * 3000,                             # oversized (sequential path), accepted
+        good + " " * 3000 + "x",                       # oversized with trailing content
+        good + "\n" * 200,                             # more newlines than the warp keeps
+        good.replace(lines[5] + "\n", lines[5] + "\n\n"),  # an empty line inside
+        "ranmar24 v1",                                 # header only
+        good[:-30],                                    # cut inside the last line
     ]
     texts = [b.encode() for b in bad]
     offs = np.cumsum([0] + [len(t) for t in texts]).astype(np.int64)
@@ -88,7 +95,7 @@ def test_from_text_errors_match_reference(refvec):
     for k, b in enumerate(bad):
         assert err[k] == _host_error_line(b), (k, b[:40])
     ok = [k for k, e in enumerate(err) if e == 0]
-    assert ok == [11, 12]
+    assert ok == [11, 12, 14, 15, 17]
     host = rb.states_to_host(states)
     for k in ok:
         assert host[k:k + 1].tobytes() == rb.from_text(bad[k]).tobytes()
