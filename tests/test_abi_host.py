@@ -107,3 +107,28 @@ def test_device_entry_points_fail_loudly_without_gpu():
     # ctx creation reports a CUDA error instead of computing anything on the CPU
     with pytest.raises(rb.RanmarError):
         rb.Context(0)
+
+
+def test_device_entry_points_validate_arguments_first():
+    # argument errors are reported as RANMAR_EINVAL before any device work, so
+    # they behave the same with or without a GPU (the reference throws
+    # std::invalid_argument at the same places, jump.hpp:111-112)
+    import ctypes as C
+    lib = rb.lib()
+    EINVAL = rb.EINVAL
+    vp = C.c_void_p(0x1000)  # never dereferenced: the checks come first
+    assert lib.ranmar_generate_u32_dev(None, 4, 4, vp, None) == EINVAL
+    assert lib.ranmar_generate_f32_dev(vp, 4, 4, None, None) == EINVAL
+    assert lib.ranmar_consume_dev(vp, 4, 4, None, vp, None) == EINVAL
+    assert lib.ranmar_gaussian_f64_dev(None, 4, 3, 2, vp, None) == EINVAL
+    assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, 1, 1.0, 7, None) == EINVAL
+    assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, -1, 1.0, 0, None) == EINVAL
+    assert lib.ranmar_langevin_dev(vp, 4, None, vp, vp, None, 1, vp, vp, 1, 1.0, 0, None) == EINVAL
+    s = rb.init(1)
+    j = rb._JumpCount()
+    assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 4, vp, vp, 1 << 20,
+                                       None) == EINVAL  # J = 0 (jump.hpp:112)
+    j.limb[0] = 5
+    assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 0, vp, vp, 1 << 20,
+                                       None) == EINVAL  # n = 0 (jump.hpp:111)
+    assert lib.ranmar_last_error().decode()  # every failure leaves a message

@@ -335,6 +335,28 @@ def test_gaussian_shapes(oracle, per_step, steps):
 
 # ------------------------------------------------------ invariants, host API
 
+def test_zero_sized_calls_are_no_ops(oracle):
+    # n = 0 or zero outputs per stream: OK, nothing launched on garbage, states unchanged
+    d = rb.states_to_device(random_states(3, 4, oracle))
+    d0 = d.clone()
+    empty = d[:0]
+    assert rb.generate(empty, 100, "u32").numel() == 0
+    assert rb.generate(d, 0, "f32").numel() == 0
+    sums, hist = rb.consume(d, 0)
+    assert int(sums.abs().sum()) == 0 and int(hist.abs().sum()) == 0
+    assert rb.jump_dev(empty, 2**40).numel() == 0
+    g = rb.gauss_states_from(d)
+    assert rb.gaussian(g, 3, 0).numel() == 0 and rb.gaussian(g[:0], 3, 5).numel() == 0
+    assert torch.equal(d, d0) and torch.equal(g[:, :rb.STATE_WORDS], d0)
+    f = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    gf = torch.zeros(2, dtype=torch.float64, device="cuda")
+    rb.langevin(g[:0], f, f, torch.zeros(0, dtype=torch.int32, device="cuda"), gf, gf, 1.0)
+    text, off = rb.to_text_dev(empty)
+    assert off.numel() == 1
+    torch.cuda.synchronize()
+    assert rb.device_status() == 0
+
+
 def test_bad_state_is_flagged(oracle):
     s = oracle.init(1)
     s["j"] = 0  # separation != 64
