@@ -132,3 +132,8 @@ def test_device_entry_points_validate_arguments_first():
     assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 0, vp, vp, 1 << 20,
                                        None) == EINVAL  # n = 0 (jump.hpp:111)
     assert lib.ranmar_last_error().decode()  # every failure leaves a message
+    j.limb[0], j.limb[3] = 0, 1 << 62  # J = 2^254: stream 4 would need 2^256
+    assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 5, vp, vp, 1 << 30,
+                                       None) == rb.ERANGE
+    assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 4, vp, vp, 16,
+                                       None) == rb.ENOMEM  # workspace too small
