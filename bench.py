@@ -458,7 +458,15 @@ def run_ours(args, rank, world, local):
         extras["config4"] = {"workload": f"{n4} streams x 2^20 uniforms consumed per rank "
                                          "(make_streams(42, 2^64) + per-stream u64 sum + 256-bin hist)",
                              "uniforms_per_s": n4 * C4["per"] * world / (ms4 * 1e-3), "ms": ms4}
-        del st4, ws4, sums4, hist4
+        # after timing: all-gather the per-stream sums, all-reduce the histogram
+        from paper_2512_00093_b200.shard import allgather_tensor, allreduce_sum
+        all_sums = allgather_tensor(sums4)
+        hist_tot = allreduce_sum(hist4.to(torch.int64).sum(dim=0))
+        assert int(hist_tot.sum()) == n4 * C4["per"] * world  # every uniform counted once
+        extras["config4"]["gathered"] = {
+            "streams": int(all_sums.numel()), "sum_of_sums": int(all_sums.sum()) & ((1 << 64) - 1),
+            "hist_total": int(hist_tot.sum())}
+        del st4, ws4, sums4, hist4, all_sums
 
     # ---- config 5: gaussians ----
     if not args.quick:

@@ -41,3 +41,24 @@ def gather_u64(values: Sequence[int], device=None) -> List[List[int]]:
     out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(out, t)
     return [[v & ((1 << 64) - 1) for v in o.tolist()] for o in out]
+
+
+def allgather_tensor(t):
+    """All-gather a tensor from every rank (after the timed region only): the
+    per-stream u64 sums of config 4, 8 B x streams per rank.
+    Returns the concatenation in rank order; the tensor itself at world size 1."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return t
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t.contiguous())
+    return torch.cat(out)
+
+
+def allreduce_sum(t):
+    """Sum-reduce a tensor over ranks in place (the 256-bin histogram total)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t

@@ -80,3 +80,47 @@ def test_stream_range_properties():
             assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
     with pytest.raises(ValueError):
         stream_range(10, 2, 2)
+
+
+def _worker_tensors(rank, world, port, n, per, result_q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle.bind import Oracle
+    from paper_2512_00093_b200.shard import allgather_tensor, allreduce_sum, weak_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        first, cnt = weak_range(n, rank)
+        sums, hist = orc.consume(orc.make_streams(orc.init(42), 2**64, cnt, first=first), per)
+        all_sums = allgather_tensor(torch.from_numpy(sums.view(np.int64).copy()))
+        tot = allreduce_sum(torch.from_numpy(hist.astype(np.int64)).sum(dim=0))
+        if rank == 0:
+            result_q.put((all_sums.numpy().view(np.uint64).tolist(), tot.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sums_gather_and_histogram_reduce(oracle):
+    # bench.py's config-4 collectives after timing: all-gather of
+    # the per-stream u64 sums, all-reduce of the 256-bin histogram
+    world, n, per = 2, 5, 700
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tensors, args=(r, world, port, n, per, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    sums, tot = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    exp_sums, exp_hist = oracle.consume(
+        oracle.make_streams(oracle.init(42), 2**64, world * n), per)
+    assert sums == [int(x) for x in exp_sums]
+    assert tot == exp_hist.astype(np.int64).sum(axis=0).tolist()
+    assert sum(tot) == world * n * per
