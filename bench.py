@@ -492,6 +492,13 @@ def run_ours(args, rank, world, local):
         extras["config5"] = {"workload": "2^24 atoms x 3 gaussian() x 100 steps per rank, fp64 out",
                              "gaussians_per_s": out5.numel() * world / (ms5 * 1e-3), "ms": ms5,
                              "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9}
+        # after timing: every rank's deviate sum and sum of squares, all-gathered
+        from paper_2512_00093_b200.shard import allgather_tensor
+        mom = torch.stack([out5.sum(dtype=torch.float64), (out5 * out5).sum(dtype=torch.float64)])
+        mom = allgather_tensor(mom).view(-1, 2)
+        cnt5 = out5.numel() * world
+        extras["config5"]["gathered"] = {"mean": float(mom[:, 0].sum()) / cnt5,
+                                         "mean_square": float(mom[:, 1].sum()) / cnt5}
 
         # the same 100 steps launched one MD step at a time (3 deviates per atom
         # per launch: states stepped in place, K6), then the fused consumer
