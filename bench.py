@@ -536,6 +536,18 @@ def run_ours(args, rank, world, local):
             # (uniform: 3 uniforms; gaussian: ~3.8 uniforms, counted as 3)
             lang[name] = {"ms_per_step": ms_l, "atoms_per_s": n5 * world / (ms_l * 1e-3),
                           "algorithmic_GB_per_s": n5 * 136 / (ms_l * 1e-3) / 1e9}
+        # the same uniform-noise consumer on a stream bank (slot-major, coalesced)
+        gf1, gf2 = rb.langevin_factors([0.0, 1.0], 0.1, 0.005, noise=rb.NOISE_UNIFORM)
+        d1, d2 = torch.from_numpy(gf1).to(dev), torch.from_numpy(gf2).to(dev)
+        bank = rb.bank_from_states(g5w)
+        tb = [0]
+
+        def bank_step():
+            tb[0] = rb.langevin_bank(bank, tb[0], vel, frc, typ, d1, d2, 1.0, stream=stream)
+        ms_b = timed(bank_step, 20)
+        lang["uniform_bank"] = {"ms_per_step": ms_b, "atoms_per_s": n5 * world / (ms_b * 1e-3),
+                                "algorithmic_GB_per_s": n5 * 120 / (ms_b * 1e-3) / 1e9}
+        del bank
         extras["langevin"] = lang
         del g5, g5w, vel, frc, typ
 

@@ -169,6 +169,25 @@ int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double*
                         int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
                         int32_t n_types, double tsqrt, int noise, void* stream);
 
+/* Stream bank: n streams transposed slot-major (99 u32 words per stream:
+ * 97 ring slots, v, the initial cursor) for consumers that draw the same
+ * number of outputs from every stream per launch, so every access of a launch
+ * is coalesced. t = outputs drawn from each stream since from_states; the
+ * round trip to_states(from_states(S), t) is byte-identical to t calls of
+ * step() on each state. ranmar_langevin_bank_dev is ranmar_langevin_dev with
+ * RANMAR_NOISE_UNIFORM, no mask, on a bank (every stream draws 3 outputs; an
+ * atom with a bad type keeps its force, is flagged, and still draws); it
+ * returns with the bank at t + 3. */
+uint64_t ranmar_bank_words(uint64_t n);
+int ranmar_bank_from_states_dev(const ranmar_state* d_states, uint64_t n, uint32_t* d_bank,
+                                void* stream);
+int ranmar_bank_to_states_dev(const uint32_t* d_bank, uint64_t n, uint64_t t,
+                              ranmar_state* d_states, void* stream);
+int ranmar_langevin_bank_dev(uint32_t* d_bank, uint64_t n_atoms, uint64_t t, const double* d_v,
+                             double* d_f, const int32_t* d_type, const double* d_gfactor1,
+                             const double* d_gfactor2, int32_t n_types, double tsqrt,
+                             void* stream);
+
 /* Diagnostic: compares gaussian()'s branch-free fp64 divide / sqrt with the
  * CUDA library's correctly rounded ones on n operand sets drawn from seed
  * (rsq = s / 2^46); adds the number of bitwise mismatches to *d_mismatches. */

@@ -86,6 +86,10 @@ def lib() -> C.CDLL:
         "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
         "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
+        "ranmar_bank_words": (u64, [u64]),
+        "ranmar_bank_from_states_dev": (i32, [vp, u64, vp, vp]),
+        "ranmar_bank_to_states_dev": (i32, [vp, u64, u64, vp, vp]),
+        "ranmar_langevin_bank_dev": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, i32, C.c_double, vp]),
         "ranmar_langevin_dev": (i32, [vp, u64, vp, vp, vp, vp, i32, vp, vp, i32, C.c_double,
                                       i32, vp]),
         "ranmar_device_status": (i32, [C.POINTER(C.c_uint32), i32]),
@@ -383,6 +387,37 @@ def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int 
                                      _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
                                      float(tsqrt), noise, _stream_ptr(stream)))
     return f
+
+
+def bank_from_states(states, stream=None):
+    """[n, 100] (or gauss [n, 104]) state tensor -> stream bank [99, n] (int32 words)."""
+    torch = _torch()
+    n = states.shape[0]
+    src = states if states.shape[1] == STATE_WORDS else states[:, :STATE_WORDS].contiguous()
+    bank = torch.empty((99, n), dtype=torch.int32, device=states.device)
+    _check(lib().ranmar_bank_from_states_dev(_dptr(src), n, _dptr(bank), _stream_ptr(stream)))
+    return bank
+
+
+def bank_to_states(bank, t: int, out=None, stream=None):
+    """Stream bank at t outputs per stream -> [n, 100] states (as t calls of step())."""
+    torch = _torch()
+    n = bank.shape[1]
+    if out is None:
+        out = torch.empty((n, STATE_WORDS), dtype=torch.int32, device=bank.device)
+    _check(lib().ranmar_bank_to_states_dev(_dptr(bank), n, t, _dptr(out), _stream_ptr(stream)))
+    return out
+
+
+def langevin_bank(bank, t: int, v, f, types, gfactor1, gfactor2, tsqrt: float, stream=None) -> int:
+    """Uniform-noise Langevin on a stream bank (every atom draws 3); returns t + 3."""
+    n = bank.shape[1]
+    if tuple(v.shape) != (n, 3) or tuple(f.shape) != (n, 3) or types.shape[0] != n:
+        raise ValueError("langevin_bank: v, f must be [n_atoms, 3] and types [n_atoms]")
+    _check(lib().ranmar_langevin_bank_dev(_dptr(bank), n, t, _dptr(v), _dptr(f), _dptr(types),
+                                          _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
+                                          float(tsqrt), _stream_ptr(stream)))
+    return t + 3
 
 
 def fp64_selfcheck(n: int, seed: int = 1) -> int:

@@ -145,6 +145,92 @@ __global__ void __launch_bounds__(256)
     gs->has_saved = has ? 1u : 0u;
 }
 
+// ---- Stream bank: n streams transposed slot-major for consumers that draw the
+// same number of outputs from every stream per launch (uniform-noise Langevin).
+// Word layout (u32): rows 0..96 hold slot s of every stream (slot s = the
+// latest x_m with m = s mod 97, loaded in canonical order X[s] =
+// lane[(i0 - s) mod 97] as in K2), row 97 holds v, row 98 the stream's i0.
+// After t outputs slot s still maps back to ring position (i0 - s) mod 97 and
+// the cursor is (i0 - t) mod 97, so the round trip is byte-identical to t
+// calls of step(). A launch that draws 3 outputs touches rows t, t+1, t+2 and
+// their lag partners (mod 97) for all streams: every access is coalesced and
+// DRAM moves ~44 B of state per stream-step instead of the ~370 B of sectors
+// an in-place AoS update touches.
+constexpr int kBankRows = 99;
+
+__global__ void bank_from_states_kernel(const ranmar_state* __restrict__ st, uint64_t n,
+                                        uint32_t* __restrict__ bank, uint32_t* status) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const ranmar_state* r = st + a;
+    const int i0 = r->i;
+    if (!state_ok(i0, r->j, r->v)) atomicOr(status, kStatusBadState);
+    const int ic = static_cast<unsigned>(i0) < 97u ? i0 : 0;
+#pragma unroll 4
+    for (int s = 0; s < 97; ++s) {
+        const int q = ic - s;
+        bank[s * n + a] = r->lane[q < 0 ? q + 97 : q];
+    }
+    bank[97 * n + a] = r->v;
+    bank[98 * n + a] = static_cast<uint32_t>(ic);
+}
+
+__global__ void bank_to_states_kernel(const uint32_t* __restrict__ bank, uint64_t n, uint32_t t97,
+                                      ranmar_state* __restrict__ st) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    ranmar_state* r = st + a;
+    const int i0 = static_cast<int>(bank[98 * n + a]);
+#pragma unroll 4
+    for (int s = 0; s < 97; ++s) {
+        const int q = i0 - s;
+        r->lane[q < 0 ? q + 97 : q] = bank[s * n + a] & kMask;
+    }
+    int i = i0 - static_cast<int>(t97);
+    i += i < 0 ? 97 : 0;
+    r->i = i;
+    r->j = i >= 64 ? i - 64 : i + 33;
+    r->v = bank[97 * n + a];
+}
+
+// Uniform-noise Langevin on a bank: every stream draws 3 outputs (an atom with
+// a type outside [0, n_types] is flagged and its force left alone, but its
+// stream still advances, so the bank stays in lockstep).
+__global__ void __launch_bounds__(256)
+    langevin_bank_kernel(uint32_t* __restrict__ bank, uint64_t n, uint32_t s0,
+                         const double* __restrict__ vel, double* __restrict__ force,
+                         const int32_t* __restrict__ type, const double* __restrict__ gf1,
+                         const double* __restrict__ gf2, int32_t n_types, double tsqrt,
+                         uint32_t* status) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const int32_t t = type[a];
+    const bool ok = t >= 0 && t <= n_types;
+    if (!ok) atomicOr(status, kStatusBadType);
+    uint32_t v = bank[97 * n + a];
+    double r[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        int sl = static_cast<int>(s0) + d;
+        sl -= sl >= 97 ? 97 : 0;
+        const int pr = sl >= 33 ? sl - 33 : sl + 64;  // (sl + 64) mod 97: x_{m-33}
+        uint32_t* xs = bank + sl * n + a;
+        const uint32_t x = (*xs - bank[pr * n + a]) & kMask;
+        *xs = x;
+        v = add_mod_m(v, kStepA);
+        r[d] = __dsub_rn(__dmul_rn(static_cast<double>((x - v) & kMask), 0x1p-24), 0.5);
+    }
+    bank[97 * n + a] = v;
+    if (!ok) return;
+    const double g1 = gf1[t];
+    const double g2 = __dmul_rn(gf2[t], tsqrt);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double fd = __dadd_rn(__dmul_rn(g1, vel[3 * a + d]), __dmul_rn(g2, r[d]));
+        force[3 * a + d] = __dadd_rn(force[3 * a + d], fd);
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_langevin(ranmar_gauss_state* d_g, uint64_t n_atoms, const double* d_v,
@@ -174,6 +260,36 @@ cudaError_t launch_gaussian_inplace(ranmar_gauss_state* d_g, uint64_t n_atoms, u
     count_launch();
     gaussian_inplace_kernel<<<blocks, 256, 0, stream>>>(d_g, n_atoms, per_step, steps, d_out,
                                                         status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bank_from_states(const ranmar_state* d_states, uint64_t n, uint32_t* d_bank,
+                                   uint32_t* status, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    bank_from_states_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+        d_states, n, d_bank, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bank_to_states(const uint32_t* d_bank, uint64_t n, uint64_t t,
+                                  ranmar_state* d_states, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    bank_to_states_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+        d_bank, n, static_cast<uint32_t>(t % 97), d_states);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_langevin_bank(uint32_t* d_bank, uint64_t n, uint64_t t, const double* d_v,
+                                 double* d_f, const int32_t* d_type, const double* d_gf1,
+                                 const double* d_gf2, int32_t n_types, double tsqrt,
+                                 uint32_t* status, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    langevin_bank_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+        d_bank, n, static_cast<uint32_t>(t % 97), d_v, d_f, d_type, d_gf1, d_gf2, n_types, tsqrt,
+        status);
     return cudaGetLastError();
 }
 

@@ -44,6 +44,12 @@ cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, d
 cudaError_t launch_langevin(ranmar_gauss_state*, uint64_t, const double*, double*, const int32_t*,
                             const int32_t*, int32_t, const double*, const double*, int32_t, double,
                             int, uint32_t*, cudaStream_t);
+cudaError_t launch_bank_from_states(const ranmar_state*, uint64_t, uint32_t*, uint32_t*,
+                                   cudaStream_t);
+cudaError_t launch_bank_to_states(const uint32_t*, uint64_t, uint64_t, ranmar_state*, cudaStream_t);
+cudaError_t launch_langevin_bank(uint32_t*, uint64_t, uint64_t, const double*, double*,
+                                 const int32_t*, const double*, const double*, int32_t, double,
+                                 uint32_t*, cudaStream_t);
 cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
@@ -627,6 +633,40 @@ int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double*
                                 d_gfactor2, n_types, tsqrt, noise == RANMAR_NOISE_GAUSSIAN, status,
                                 static_cast<cudaStream_t>(stream)),
             "langevin_kernel launch");
+    return RANMAR_OK;
+}
+
+uint64_t ranmar_bank_words(uint64_t n) { return 99 * n; }
+
+int ranmar_bank_from_states_dev(const ranmar_state* d_states, uint64_t n, uint32_t* d_bank,
+                                void* stream) {
+    if (n && (!d_states || !d_bank)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_bank_from_states(d_states, n, d_bank, status,
+                                        static_cast<cudaStream_t>(stream)),
+            "bank_from_states_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_bank_to_states_dev(const uint32_t* d_bank, uint64_t n, uint64_t t,
+                              ranmar_state* d_states, void* stream) {
+    if (n && (!d_states || !d_bank)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_CUDA(rb::launch_bank_to_states(d_bank, n, t, d_states, static_cast<cudaStream_t>(stream)),
+            "bank_to_states_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_langevin_bank_dev(uint32_t* d_bank, uint64_t n_atoms, uint64_t t, const double* d_v,
+                             double* d_f, const int32_t* d_type, const double* d_gfactor1,
+                             const double* d_gfactor2, int32_t n_types, double tsqrt,
+                             void* stream) {
+    if (n_types < 0) return fail(RANMAR_EINVAL, "ranmar_langevin_bank_dev: n_types < 0");
+    if (n_atoms && (!d_bank || !d_v || !d_f || !d_type || !d_gfactor1 || !d_gfactor2))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_langevin_bank(d_bank, n_atoms, t, d_v, d_f, d_type, d_gfactor1, d_gfactor2,
+                                     n_types, tsqrt, status, static_cast<cudaStream_t>(stream)),
+            "langevin_bank_kernel launch");
     return RANMAR_OK;
 }
 

@@ -113,3 +113,48 @@ def test_gaussian_inplace_boundary(oracle, per_step, steps):
         exp = oracle.gaussian_fill(g, per_step, steps)
         assert out.tobytes() == exp.tobytes()
     assert dg.cpu().numpy().view(GAUSS_DTYPE).reshape(-1).tobytes() == g.tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 300, 4099])
+def test_stream_bank_round_trip_and_langevin(oracle, n):
+    # bank layout (ranmar_bank_*): to_states(from_states(S), t) is byte-identical
+    # to t calls of step(); langevin_bank equals the AoS consumer (uniform
+    # noise, no mask) bit for bit, across the slot wrap at t = 97
+    g, v, f, rng = _atoms(n, 500 + n, oracle)
+    states = torch.from_numpy(g["s"].copy().view(np.int32).reshape(n, rb.STATE_WORDS)).cuda()
+    bank = rb.bank_from_states(states)
+    assert torch.equal(rb.bank_to_states(bank, 0), states)
+    mass = np.array([0.0, 1.0, 4.0])
+    gf1, gf2 = rb.langevin_factors(mass, 0.2, 0.01)
+    types = rng.integers(1, 3, n).astype(np.int32)
+    dv, df = torch.from_numpy(v).cuda(), torch.from_numpy(f.copy()).cuda()
+    dt_, d1, d2 = torch.from_numpy(types).cuda(), torch.from_numpy(gf1).cuda(), torch.from_numpy(gf2).cuda()
+    fo = f.copy()
+    t = 0
+    for step in range(40):  # 120 outputs per stream: the slots wrap past 97
+        t = rb.langevin_bank(bank, t, dv, df, dt_, d1, d2, 1.3)
+        oracle.langevin(g, v, fo, types, gf1, gf2, 1.3, rb.NOISE_UNIFORM)
+    assert t == 120
+    assert df.cpu().numpy().tobytes() == fo.tobytes()
+    back = rb.bank_to_states(bank, t).cpu().numpy().view(STATE_DTYPE).reshape(-1)
+    assert back.tobytes() == g["s"].tobytes()
+    assert rb.device_status() == 0
+
+
+def test_stream_bank_bad_type_keeps_lockstep(oracle):
+    g, v, f, _ = _atoms(64, 77, oracle)
+    states = torch.from_numpy(g["s"].copy().view(np.int32).reshape(64, rb.STATE_WORDS)).cuda()
+    bank = rb.bank_from_states(states)
+    types = np.ones(64, np.int32)
+    types[5] = 9
+    gf1, gf2 = rb.langevin_factors([0.0, 1.0], 0.2, 0.01)
+    df = torch.from_numpy(f.copy()).cuda()
+    rb.device_status(clear=True)
+    rb.langevin_bank(bank, 0, torch.from_numpy(v).cuda(), df, torch.from_numpy(types).cuda(),
+                     torch.from_numpy(gf1).cuda(), torch.from_numpy(gf2).cuda(), 1.0)
+    assert rb.device_status(clear=True) & 4
+    assert df[5].cpu().numpy().tobytes() == f[5].tobytes()  # force untouched
+    back = rb.bank_to_states(bank, 3).cpu().numpy().view(STATE_DTYPE).reshape(-1)
+    s5 = g["s"][5:6].copy()
+    oracle.step_n(s5, 3)  # the stream still advanced by 3
+    assert back[5:6].tobytes() == s5.tobytes()
