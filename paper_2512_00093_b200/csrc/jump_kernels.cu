@@ -519,7 +519,7 @@ __global__ void put_state_kernel(ranmar_state s, ranmar_state* dst) {
 //  * results go straight from registers to HBM as 16-B stores (no staging).
 constexpr int kBulkWarps = 12;
 constexpr int kBulkThreads = 32 * kBulkWarps;
-constexpr size_t kBulkSmem = (size_t(kPolyN) * kRows + 2 * kWAnchor + 2 * kRows) * 4;
+constexpr size_t kBulkSmem = (size_t(kPolyN) * kRows + 3 * kWAnchor + 3 * kRows) * 4 + 3 * 8;
 
 struct BulkArgs {
     const uint32_t* W1;   // anchors' extensions, H x kWAnchor
@@ -547,42 +547,72 @@ __device__ __forceinline__ void bulk_tail(const BulkArgs& args, uint32_t* C0, ui
     *reinterpret_cast<uint4*>(args.out[row0 + row].lane + 96) = make_uint4(a0 & kMask, 96u, 32u, v);
 }
 
+// Split-phase CTA barrier on an mbarrier: every thread arrives once per anchor
+// (release) and waits (acquire) only where a later anchor needs that anchor's
+// shared-memory writes, so warps are never held at a full barrier per anchor.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+}
+
+// Anchors are processed in a 3-deep ring: iteration `it` computes anchor it
+// from W[it % 3], prefetches anchor it + 2 into W[(it + 2) % 3] (after waiting
+// for the end of it - 1, the last reader of that buffer), adds its column-0
+// partials into C0[it % 3], and arrives on bar[it % 3]. The record tails of
+// anchor it are written at iteration it + 2, after waiting for its end.
 __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_constant__ BulkArgs args) {
     extern __shared__ uint4 sm4[];
     uint32_t* Tt = reinterpret_cast<uint32_t*>(sm4);  // [97][128]
-    uint32_t* Wb = Tt + kPolyN * kRows;               // [2][196]
-    uint32_t* C0 = Wb + 2 * kWAnchor;                 // [2][128] column-0 sums
+    uint32_t* Wb = Tt + kPolyN * kRows;               // [3][196]
+    uint32_t* C0 = Wb + 3 * kWAnchor;                 // [3][128] column-0 sums
+    uint64_t* bar = reinterpret_cast<uint64_t*>(C0 + 3 * kRows);  // [3]
     const int t = threadIdx.x;
     const int g = t >> 5, rg = t & 31;
     const int m0 = 89 - 8 * g;
+    const uint64_t G = gridDim.x;
 
     {   // T^T tile, loaded once per CTA
         const uint4* src = reinterpret_cast<const uint4*>(args.Tt);
         for (int x = t; x < kPolyN * kRows / 4; x += kBulkThreads) sm4[x] = src[x];
     }
-    uint64_t h = blockIdx.x;
-    if (h < args.H && t < 193) Wb[t] = args.W1[h * kWAnchor + t];
-    if (t < 2 * kRows) C0[t] = 0;
+    const uint64_t h0 = blockIdx.x;
+    for (int q = 0; q < 2; ++q)
+        if (h0 + q * G < args.H && t < 193) Wb[q * kWAnchor + t] = args.W1[(h0 + q * G) * kWAnchor + t];
+    if (t < 3 * kRows) C0[t] = 0;
+    if (t == 0)
+        for (int q = 0; q < 3; ++q) mbar_init(bar + q, kBulkThreads);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
+    // end of iteration k: bar[k % 3], phase parity (k / 3) & 1
+    auto wait_end = [&](int k) { mbar_wait(bar + k % 3, static_cast<uint32_t>((k / 3) & 1)); };
     const int crow = t & (kRows - 1), cpart = t >> 7;  // column 0: row, third of the terms
     const int cj0 = 33 * cpart, cj1 = cpart == 2 ? kPolyN : cj0 + 33;
-    uint64_t hprev = ~0ull;
-    for (int it = 0; h < args.H; ++it, h += gridDim.x) {
-        const uint32_t* W = Wb + (it & 1) * kWAnchor;
-        if (hprev != ~0ull && t < kRows) bulk_tail(args, C0 + ((it & 1) ^ 1) * kRows, hprev, t);
-        {   // column 0 partial sums (the buffer was zeroed before the last barrier)
-            uint32_t a0 = 0;
-#pragma unroll 11
-            for (int j = cj0; j < cj1; ++j) a0 += Tt[j * kRows + crow] * W[j];
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(static_cast<uint32_t>(
-                             __cvta_generic_to_shared(C0 + (it & 1) * kRows + crow))),
-                         "r"(a0)
-                         : "memory");
+    int it = 0;
+    for (uint64_t h = h0; h < args.H; ++it, h += G) {
+        const int slot = it % 3;
+        const uint32_t* W = Wb + slot * kWAnchor;
+        if (it >= 2) {
+            wait_end(it - 2);  // W[slot] (prefetched in it - 2) and C0 of anchor it - 2 are complete
+            if (t < kRows) bulk_tail(args, C0 + ((it - 2) % 3) * kRows, h - 2 * G, t);
         }
-        const uint64_t hn = h + gridDim.x;
-        if (hn < args.H && t < 193) Wb[((it + 1) & 1) * kWAnchor + t] = args.W1[hn * kWAnchor + t];
-
         uint32_t acc[4][8];
         uint32_t win[8];
 #pragma unroll
@@ -629,12 +659,26 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
         }
         if (skip0 && t < 100)
             reinterpret_cast<uint32_t*>(args.out)[t] = reinterpret_cast<const uint32_t*>(&args.base)[t];
-        hprev = h;
-        __syncthreads();
+        // W[(it + 2) % 3] and C0[slot]: their last readers / the tail that zeroed
+        // C0[slot] ran in iteration it - 1
+        if (it >= 1) wait_end(it - 1);
+        const uint64_t hn = h + 2 * G;
+        if (hn < args.H && t < 193) Wb[((it + 2) % 3) * kWAnchor + t] = args.W1[hn * kWAnchor + t];
+        {   // column 0 partial sums of this anchor
+            uint32_t a0 = 0;
+#pragma unroll 11
+            for (int j = cj0; j < cj1; ++j) a0 += Tt[j * kRows + crow] * W[j];
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(static_cast<uint32_t>(
+                             __cvta_generic_to_shared(C0 + slot * kRows + crow))),
+                         "r"(a0)
+                         : "memory");
+        }
+        mbar_arrive(bar + slot);
     }
-    if (hprev != ~0ull && t < kRows) {
-        const int it_last = static_cast<int>((hprev - blockIdx.x) / gridDim.x);
-        bulk_tail(args, C0 + (it_last & 1) * kRows, hprev, t);
+    // tails of the last two anchors
+    for (int k = it >= 2 ? it - 2 : 0; k < it; ++k) {
+        wait_end(k);
+        if (t < kRows) bulk_tail(args, C0 + (k % 3) * kRows, h0 + static_cast<uint64_t>(k) * G, t);
     }
 }
 
