@@ -51,8 +51,8 @@ __device__ __forceinline__ int line_len(const ranmar_state& s, int line) {
     if (line == 0) return 12;
     if (line == 1) return 2 + ndigits(s.i + 1) + 3 + ndigits(s.j + 1) + 1;
     if (line == 2) return 2 + ndigits(s.v) + 1;
-    const int k = line - 3;
-    return 2 + ndigits(k + 1) + 1 + ndigits(s.lane[k]) + 1;
+    const int k = line - 3;  // k + 1 <= 97: at most two digits
+    return 2 + (k + 1 >= 10 ? 2 : 1) + 1 + ndigits(s.lane[k]) + 1;
 }
 
 __device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* p) {
