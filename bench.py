@@ -368,6 +368,24 @@ def run_ours(args, rank, world, local):
         del host_out
         ctx.close()
 
+    # ---- config 1: one stream, seed 12345, 10^8 fp32 uniforms at full width ----
+    if not args.quick:
+        n1 = 10**8
+        s1 = rb.states_to_device(rb.init(12345)).to(dev)
+        out1 = torch.empty(n1, dtype=torch.float32, device=dev)
+        rb.generate_single(s1, n1, "f32", out=out1, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rb.generate_single(s1, n1, "f32", out=out1, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms1 = max_over_ranks(a.elapsed_time(b), world)
+        extras["config1"] = {"workload": "one stream (seed 12345) x 10^8 fp32, split into 8,192-output "
+                                         "substreams (make_streams) and re-joined; state ends as 10^8 x step()",
+                             "ms": ms1, "uniforms_per_s": n1 / (ms1 * 1e-3)}
+        del out1
+
     # ---- config 3: 2^20 stream starts at J = 2^120 (jump-aheads/s) ----
     if not args.quick:
         n3 = C3["n"]

@@ -140,6 +140,18 @@ int ranmar_generate_f64_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t
 int ranmar_generate_float_dev(ranmar_float_state* d_states, uint64_t n_streams,
                               uint64_t per_stream, double* d_out, void* stream);
 
+/* ONE stream, `count` outputs at full GPU width: the stream is split into
+ * substreams of 8,192 outputs starting at s_{k 8192} (make_streams), so the
+ * outputs land in order in d_out[0 .. count), and *d_state (device) ends
+ * exactly as `count` calls of step() leave it (same ring layout). d_ws:
+ * ranmar_generate_single_workspace(count) bytes (0 for count <= 8192). The
+ * state is read back to the host once (synchronises the stream). */
+size_t ranmar_generate_single_workspace(uint64_t count);
+int ranmar_generate_single_u32_dev(ranmar_state* d_state, uint64_t count, uint32_t* d_out,
+                                   void* d_ws, size_t ws_bytes, void* stream);
+int ranmar_generate_single_f32_dev(ranmar_state* d_state, uint64_t count, float* d_out,
+                                   void* d_ws, size_t ws_bytes, void* stream);
+
 /* Consume-in-kernel (no uniform is stored): per stream, the u64 sum of its
  * per_stream 24-bit outputs and a 256-bin histogram of (u >> 16);
  * d_hist is n_streams x 256 u32. States advance in place. */

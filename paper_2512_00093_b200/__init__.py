@@ -87,6 +87,9 @@ def lib() -> C.CDLL:
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
         "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
         "ranmar_bank_words": (u64, [u64]),
+        "ranmar_generate_single_workspace": (sz, [u64]),
+        "ranmar_generate_single_u32_dev": (i32, [vp, u64, vp, vp, sz, vp]),
+        "ranmar_generate_single_f32_dev": (i32, [vp, u64, vp, vp, sz, vp]),
         "ranmar_bank_from_states_dev": (i32, [vp, u64, vp, vp]),
         "ranmar_bank_to_states_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_langevin_bank_dev": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, i32, C.c_double, vp]),
@@ -387,6 +390,21 @@ def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int 
                                      _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
                                      float(tsqrt), noise, _stream_ptr(stream)))
     return f
+
+
+def generate_single(state, count: int, fmt: str = "f32", out=None, stream=None):
+    """count outputs of ONE stream (a [1, 100] CUDA state tensor, advanced in place
+    exactly as count calls of step()) computed as 8,192-output substreams."""
+    torch = _torch()
+    dt = {"u32": torch.int32, "f32": torch.float32}[fmt]
+    fn = {"u32": lib().ranmar_generate_single_u32_dev,
+          "f32": lib().ranmar_generate_single_f32_dev}[fmt]
+    if out is None:
+        out = torch.empty(count, dtype=dt, device=state.device)
+    wsb = int(lib().ranmar_generate_single_workspace(count))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=state.device)
+    _check(fn(_dptr(state), count, _dptr(out), _dptr(ws), wsb, _stream_ptr(stream)))
+    return out
 
 
 def bank_from_states(states, stream=None):

@@ -150,9 +150,38 @@ __global__ void __launch_bounds__(32 * kGenWarps)
     });
 }
 
+// One stream generated as P substreams (ranmar_generate_single_*): the final
+// state is the last substream's, re-laid in the ORIGINAL ring layout, i.e.
+// exactly what `count` calls of step() leave: canonical u[k] = lane[(i - k)
+// mod 97] is layout-independent, and lane[(i_t - k) mod 97] = u[k] with the
+// target cursor i_t = (i0 - count) mod 97 (jump.hpp:32-48).
+__global__ void relayout_kernel(const ranmar_state* __restrict__ src, ranmar_state* __restrict__ dst,
+                                int i_t) {
+    const int k = threadIdx.x;
+    if (k < 97) {
+        int q = src->i - k;
+        q += q < 0 ? 97 : 0;
+        int r = i_t - k;
+        r += r < 0 ? 97 : 0;
+        dst->lane[r] = src->lane[q];
+    }
+    if (k == 0) {
+        dst->i = i_t;
+        dst->j = i_t >= 64 ? i_t - 64 : i_t + 33;
+        dst->v = src->v;
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+
+cudaError_t launch_relayout(const ranmar_state* src, ranmar_state* dst, int i_t,
+                            cudaStream_t stream) {
+    count_launch();
+    relayout_kernel<<<1, 128, 0, stream>>>(src, dst, i_t);
+    return cudaGetLastError();
+}
 
 template <class T>
 cudaError_t launch_generate(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,

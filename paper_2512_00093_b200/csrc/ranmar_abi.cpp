@@ -50,6 +50,7 @@ cudaError_t launch_bank_to_states(const uint32_t*, uint64_t, uint64_t, ranmar_st
 cudaError_t launch_langevin_bank(uint32_t*, uint64_t, uint64_t, const double*, double*,
                                  const int32_t*, const double*, const double*, int32_t, double,
                                  uint32_t*, cudaStream_t);
+cudaError_t launch_relayout(const ranmar_state*, ranmar_state*, int, cudaStream_t);
 cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
@@ -584,6 +585,73 @@ int ranmar_generate_f32_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t
                                        static_cast<cudaStream_t>(stream)),
             "gen_store_kernel<f32> launch");
     return RANMAR_OK;
+}
+
+// ---- one long stream at full width: substream k starts at s_{kL} (make_streams),
+// outputs land in order, and the state ends as `count` calls of step() leave it.
+}  // extern "C"
+
+namespace {
+
+constexpr uint64_t kSingleL = 8192;  // outputs per substream
+
+uint64_t single_parts(uint64_t count) { return (count + kSingleL - 1) / kSingleL; }
+
+size_t single_ws_states(uint64_t parts) {
+    return static_cast<size_t>((parts * sizeof(ranmar_state) + 255) / 256 * 256);
+}
+
+template <class T>
+int generate_single(ranmar_state* d_state, uint64_t count, T* d_out, void* d_ws, size_t ws_bytes,
+                    void* stream, int (*gen)(ranmar_state*, uint64_t, uint64_t, T*, void*)) {
+    if (count == 0) return RANMAR_OK;
+    if (!d_state || !d_out) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    const uint64_t parts = single_parts(count);
+    if (parts == 1) return gen(d_state, 1, count, d_out, stream);
+    const size_t need = ranmar_generate_single_workspace(count);
+    if (!d_ws) return fail(RANMAR_EINVAL, "ranmar: null workspace");
+    if (ws_bytes < need) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ranmar_state base;
+    RB_CUDA(cudaMemcpyAsync(&base, d_state, sizeof base, cudaMemcpyDeviceToHost, s), "D2H state");
+    RB_CUDA(cudaStreamSynchronize(s), "sync");
+    if (!host_state_ok(base))
+        return fail(RANMAR_ESTATE, "ranmar: state violates cursor/residue invariants");
+    ranmar_state* sub = static_cast<ranmar_state*>(d_ws);
+    char* ws2 = static_cast<char*>(d_ws) + single_ws_states(parts);
+    ranmar_jump_count J = {{kSingleL, 0, 0, 0}};
+    if (int rc = ranmar_make_streams_dev(&base, &J, 0, parts, sub, ws2, ws_bytes - single_ws_states(parts),
+                                         stream))
+        return rc;
+    if (int rc = gen(sub, parts - 1, kSingleL, d_out, stream)) return rc;
+    const uint64_t last = count - (parts - 1) * kSingleL;
+    if (int rc = gen(sub + parts - 1, 1, last, d_out + (parts - 1) * kSingleL, stream)) return rc;
+    int i_t = static_cast<int>((static_cast<int64_t>(base.i) - static_cast<int64_t>(count % 97)) % 97);
+    i_t += i_t < 0 ? 97 : 0;
+    RB_CUDA(rb::launch_relayout(sub + parts - 1, d_state, i_t, s), "relayout_kernel launch");
+    return RANMAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ranmar_generate_single_workspace(uint64_t count) {
+    const uint64_t parts = single_parts(count);
+    if (parts <= 1) return 0;
+    return single_ws_states(parts) + ranmar_make_streams_workspace(parts);
+}
+
+int ranmar_generate_single_u32_dev(ranmar_state* d_state, uint64_t count, uint32_t* d_out,
+                                   void* d_ws, size_t ws_bytes, void* stream) {
+    return generate_single<uint32_t>(d_state, count, d_out, d_ws, ws_bytes, stream,
+                                     ranmar_generate_u32_dev);
+}
+
+int ranmar_generate_single_f32_dev(ranmar_state* d_state, uint64_t count, float* d_out,
+                                   void* d_ws, size_t ws_bytes, void* stream) {
+    return generate_single<float>(d_state, count, d_out, d_ws, ws_bytes, stream,
+                                  ranmar_generate_f32_dev);
 }
 
 int ranmar_generate_f64_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,

@@ -194,6 +194,29 @@ def test_config1_integer_and_float(refvec, oracle):
     assert (f[:10**6].cpu().numpy().astype(np.float64) == fl).all()
 
 
+@pytest.mark.parametrize("count", [1, 97, 8192, 8193, 20000, 1_000_007])
+def test_generate_single_equals_one_warp(oracle, count):
+    # one stream split into 8,192-output substreams: same outputs as the
+    # single-warp path, and the state ends byte-identical to count x step()
+    base = random_states(1, count, oracle)
+    a = rb.states_to_device(base)
+    b = rb.states_to_device(base)
+    for fmt in ("u32", "f32"):
+        ua = rb.generate(a, count, fmt)
+        ub = rb.generate_single(b, count, fmt)
+        assert torch.equal(ua, ub), fmt
+        assert torch.equal(a, b), fmt  # states after 2 x count outputs, same layout
+
+
+def test_config1_single_stream_full_width(refvec, oracle):
+    # config 1 (one stream, 10^8) through the split path: the reference's summary
+    c = refvec["c1_seed12345_1e8"]
+    d = rb.states_to_device(oracle.init(12345))
+    u64 = rb.generate_single(d, 10**8, "u32").to(torch.int64) & 0xFFFFFFFF
+    assert int(u64.sum()) == c["sum"] and int(u64[-1]) == c["last"]
+    assert rb.states_to_host(d).tobytes() == state_from_json(c["final_state"]).tobytes()
+
+
 def test_config2_scaled(oracle):
     # config 2 at 1/256 of the streams: make_streams(12345, 2^40, 256), 65536 fp32 each
     states = rb.make_streams(12345, 2**40, 256)
