@@ -852,7 +852,8 @@ constexpr size_t kChunkBytes = size_t(512) << 20;  // output bytes per pipelined
 
 template <class T>
 int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream, T* h_out,
-                 int (*gen)(ranmar_state*, uint64_t, uint64_t, T*, void*)) {
+                 int (*gen)(ranmar_state*, uint64_t, uint64_t, T*, void*),
+                 int (*single)(ranmar_state*, uint64_t, T*, void*, size_t, void*)) {
     if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
     c->h2d = c->d2h = 0;
     if (n == 0) return RANMAR_OK;
@@ -862,6 +863,31 @@ int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per
             return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
                                            " violates cursor/residue invariants");
     RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    if (n == 1 && ranmar_generate_single_workspace(per_stream) > 0) {
+        // one long stream: full width through substreams (ranmar_generate_single_*)
+        const size_t bytes = per_stream * sizeof(T);
+        if (int rc = ctx_states(c, 1)) return rc;
+        if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], bytes)) return rc;
+        if (int rc = ctx_reserve(&c->dws, &c->dws_bytes, ranmar_generate_single_workspace(per_stream)))
+            return rc;
+        RB_CUDA(cudaMemcpyAsync(c->dstates, h_states, sizeof(ranmar_state), cudaMemcpyHostToDevice,
+                                c->st[0]),
+                "H2D state");
+        if (int rc = single(c->dstates, per_stream, static_cast<T*>(c->dbuf[0]), c->dws, c->dws_bytes,
+                            c->st[0]))
+            return rc;
+        RB_CUDA(cudaMemcpyAsync(h_out, c->dbuf[0], bytes, cudaMemcpyDeviceToHost, c->st[0]), "D2H output");
+        RB_CUDA(cudaMemcpyAsync(h_states, c->dstates, sizeof(ranmar_state), cudaMemcpyDeviceToHost,
+                                c->st[0]),
+                "D2H state");
+        RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
+        c->h2d = sizeof(ranmar_state);
+        c->d2h = bytes + sizeof(ranmar_state);
+        uint32_t flags = 0;
+        if (int rc = ranmar_device_status(&flags, 1)) return rc;
+        if (flags) return fail(RANMAR_ESTATE, "ranmar: a device state violated the invariants");
+        return RANMAR_OK;
+    }
     const size_t stream_bytes = per_stream * sizeof(T);
     uint64_t chunk = stream_bytes ? std::max<uint64_t>(1, kChunkBytes / stream_bytes) : n;
     chunk = std::min<uint64_t>(chunk, n);
@@ -990,12 +1016,14 @@ int ranmar_ctx_jump(ranmar_ctx* c, const ranmar_state* h_in, ranmar_state* h_out
 
 int ranmar_ctx_generate_u32(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
                             uint32_t* h_out) {
-    return ctx_generate<uint32_t>(c, h_states, n, per_stream, h_out, ranmar_generate_u32_dev);
+    return ctx_generate<uint32_t>(c, h_states, n, per_stream, h_out, ranmar_generate_u32_dev,
+                                  ranmar_generate_single_u32_dev);
 }
 
 int ranmar_ctx_generate_f32(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
                             float* h_out) {
-    return ctx_generate<float>(c, h_states, n, per_stream, h_out, ranmar_generate_f32_dev);
+    return ctx_generate<float>(c, h_states, n, per_stream, h_out, ranmar_generate_f32_dev,
+                               ranmar_generate_single_f32_dev);
 }
 
 int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
