@@ -160,7 +160,8 @@ int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_
 
 /* gaussian() (no reference counterpart; Marsaglia polar, NR gasdev pairing):
  * for each atom, steps x per_step calls; d_out[(step * n_atoms + atom) *
- * per_step + c]. States (and the cached deviate) advance in place. */
+ * per_step + c] (per_step < 2^32). States (and the cached deviate) advance in
+ * place. */
 int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, void* stream);
 

@@ -76,15 +76,18 @@ __global__ void __launch_bounds__(kGT)
 
     const uint64_t G = steps * per_step;
     uint64_t q = 0;  // next deviate index of this atom
-    // out offset of deviate q: (step * n_atoms + atom) * per_step + c, advanced incrementally
-    uint64_t off = atom * per_step, c = 0;
+    // deviate q goes to out[(step * n_atoms + atom) * per_step + c]: a running pointer and a
+    // countdown to the end of the atom's row of the current step
+    double* po = out + atom * per_step;
     const uint64_t jump = (n_atoms - 1) * per_step;
+    const uint32_t row = per_step < 0xFFFFFFFFull ? static_cast<uint32_t>(per_step) : 0xFFFFFFFFu;
+    uint32_t left = row;
     auto put = [&](double x) {
-        st_cs(out + off, x);
-        ++off;
-        if (++c == per_step) {
-            c = 0;
-            off += jump;
+        st_cs(po, x);
+        ++po;
+        if (--left == 0) {
+            left = row;
+            po += jump;
         }
     };
     if (has && G > 0) {

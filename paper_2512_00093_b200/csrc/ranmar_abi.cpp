@@ -680,6 +680,8 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
                             uint64_t steps, double* d_out, void* stream) {
     if (n_atoms && (!d_g || (per_step && steps && !d_out)))
         return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (per_step >= (uint64_t(1) << 32))
+        return fail(RANMAR_EINVAL, "ranmar_gaussian_f64_dev: per_step must be below 2^32");
     RB_STATUS_PTR(status);
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
