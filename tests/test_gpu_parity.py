@@ -107,7 +107,8 @@ def test_make_streams_golden(refvec):
 
 
 @pytest.mark.parametrize("n,first", [(1, 0), (2, 0), (127, 0), (128, 0), (129, 0), (300, 0),
-                                     (1000, 0), (200, 5), (257, 1000), (1, 77)])
+                                     (1000, 0), (200, 5), (257, 1000), (1, 77),
+                                     (300, (1 << 40) + 3), (129, (1 << 61) - 200)])
 def test_make_streams_shapes(oracle, n, first):
     base = oracle.init(12345)
     got = rb.states_to_host(rb.make_streams_dev(base, 2**40, n, first=first))
