@@ -423,7 +423,13 @@ def run_ours(args, rank, world, local):
             "workload": "make_streams(init_unchecked(987654321), 2^120): 2^20 stream starts s_{kJ} per rank",
             "jump_aheads_per_s": n3 * world / (ms3 * 1e-3), "ms": ms3,
             "batched_jump_state_per_s": n3 * world / (msj * 1e-3), "batched_jump_ms": msj,
-            "macs_per_start_bulk": 97 * 97}
+            "macs_per_start_bulk": 97 * 97,
+            # whole config 3 (all launches) against the IMAD pipe at the rated SM clock
+            # (64 IMAD lanes/clk/SM x 148 SMs); the bulk kernel alone is in profiles/
+            "roofline": {"bound": "imad", "unit": "TMAC/s",
+                         "achieved": n3 * 97 * 97 / (ms3 * 1e-3) / 1e12,
+                         "peak": 64 * 148 * 1.965e9 / 1e12,
+                         "frac": n3 * 97 * 97 / (ms3 * 1e-3) / (64 * 148 * 1.965e9)}}
         # §8f row 1: export / re-import the 2^20 starts as reference text on the device
         text, off = rb.to_text_dev(st3, stream=stream)
         back, err = rb.from_text_dev(text, off, stream=stream)
@@ -509,7 +515,10 @@ def run_ours(args, rank, world, local):
         nbytes = out5.numel() * 8 + 2 * n5 * 416
         extras["config5"] = {"workload": "2^24 atoms x 3 gaussian() x 100 steps per rank, fp64 out",
                              "gaussians_per_s": out5.numel() * world / (ms5 * 1e-3), "ms": ms5,
-                             "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9}
+                             "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9,
+                             "roofline": {"bound": "hbm", "unit": "GB/s",
+                                          "achieved": nbytes / (ms5 * 1e-3) / 1e9, "peak": peak,
+                                          "frac": nbytes / (ms5 * 1e-3) / 1e9 / peak}}
         # after timing: every rank's deviate sum and sum of squares, all-gathered
         from paper_2512_00093_b200.shard import allgather_tensor
         mom = torch.stack([out5.sum(dtype=torch.float64), (out5 * out5).sum(dtype=torch.float64)])
@@ -564,7 +573,8 @@ def run_ours(args, rank, world, local):
             tb[0] = rb.langevin_bank(bank, tb[0], vel, frc, typ, d1, d2, 1.0, stream=stream)
         ms_b = timed(bank_step, 20)
         lang["uniform_bank"] = {"ms_per_step": ms_b, "atoms_per_s": n5 * world / (ms_b * 1e-3),
-                                "algorithmic_GB_per_s": n5 * 120 / (ms_b * 1e-3) / 1e9}
+                                "algorithmic_GB_per_s": n5 * 120 / (ms_b * 1e-3) / 1e9,
+                                "roofline_frac": n5 * 120 / (ms_b * 1e-3) / 1e9 / peak}
         del bank
         extras["langevin"] = lang
         del g5, g5w, vel, frc, typ
