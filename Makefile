@@ -12,7 +12,7 @@ OBJS := $(BUILD)/gen_kernels.o $(BUILD)/float_kernel.o $(BUILD)/consume_kernel.o
 HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh $(CSRC)/gauss_math.cuh
 
 .PHONY: all lib oracle ref clean sass
-all: lib oracle facade cli
+all: lib oracle facade cexample cli
 
 lib: $(LIB)
 
@@ -45,6 +45,13 @@ FACADE := tests/cpp/facade_test
 facade: $(FACADE)
 $(FACADE): tests/cpp/facade_test.cpp include/ranmar_b200.hpp $(LIB)
 	g++ -O2 -std=c++20 -Iinclude $< -L$(PKG)/lib -lranmar_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -o $@
+
+# The C ABI from plain C, run on a GPU by tests/test_facade.py
+CEXAMPLE := tests/c/abi_example
+cexample: $(CEXAMPLE)
+$(CEXAMPLE): tests/c/abi_example.c include/ranmar_b200.h $(LIB)
+	gcc -O2 -std=c11 -Wall -Werror -Iinclude -I/usr/local/cuda/include $< -L$(PKG)/lib -lranmar_b200 \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64 -o $@
 
 # GPU-backed CLI mirroring the reference's ranmar tool
 CLI := $(PKG)/bin/ranmar_b200

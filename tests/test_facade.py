@@ -33,3 +33,18 @@ def test_facade_program_on_gpu():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all checks passed" in r.stdout
+
+
+def test_c_example_compiles():
+    r = subprocess.run(["make", "-C", ROOT, "cexample"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c_example_on_gpu():
+    exe = os.path.join(ROOT, "tests", "c", "abi_example")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", ROOT, "cexample"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all checks passed" in r.stdout
