@@ -1,6 +1,6 @@
 """Small, ncu-friendly drivers for one BASELINE config each (1 GPU).
 
-    python tools/profile_case.py c2|c3|c4|c5|lang|jump [--warmup W]
+    python tools/profile_case.py c2|c3|c4|c5|lang|bank|text|jump [--warmup W]
 
 Runs W warm-up repetitions and one more of the config's GPU job, so an ncu
 capture with `-k regex:<kernel> -s W -c 1` lands on a warm launch.
@@ -19,7 +19,7 @@ import paper_2512_00093_b200 as rb  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["c2", "c3", "c4", "c5", "lang", "jump"])
+    ap.add_argument("case", choices=["c2", "c3", "c4", "c5", "lang", "bank", "text", "jump"])
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--c4-streams", type=int, default=1 << 16)
     args = ap.parse_args()
@@ -49,6 +49,24 @@ def main():
         st = rb.make_streams(42, 2**64, n)
         for _ in range(reps):
             rb.consume(st, 1 << 20)
+    elif args.case == "bank":
+        # the uniform-noise Langevin consumer on a stream bank, 2^24 atoms
+        n = 1 << 24
+        bank = rb.bank_from_states(rb.make_streams(7, 2**50, n))
+        v = torch.randn((n, 3), dtype=torch.float64, device="cuda")
+        f = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+        ty = torch.ones(n, dtype=torch.int32, device="cuda")
+        g1, g2 = rb.langevin_factors([0.0, 1.0], 0.1, 0.005)
+        d1, d2 = torch.from_numpy(g1).cuda(), torch.from_numpy(g2).cuda()
+        t = 0
+        for _ in range(reps):
+            t = rb.langevin_bank(bank, t, v, f, ty, d1, d2, 1.0)
+    elif args.case == "text":
+        # device persistence of config 3's 2^20 stream starts
+        st = rb.make_streams_dev(rb.init_unchecked(987654321), 2**120, 1 << 20)
+        for _ in range(reps):
+            text, off = rb.to_text_dev(st)
+            rb.from_text_dev(text, off)
     elif args.case == "lang":
         # fix-langevin-style consumer, one launch per MD step, 2^24 atoms (config 5 streams)
         n = 1 << 24
