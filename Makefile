@@ -9,7 +9,7 @@ CSRC := $(PKG)/csrc
 BUILD := $(PKG)/build
 LIB := $(PKG)/lib/libranmar_b200.so
 OBJS := $(BUILD)/gen_kernels.o $(BUILD)/float_kernel.o $(BUILD)/consume_kernel.o $(BUILD)/gauss_kernel.o $(BUILD)/gauss_stream_kernel.o $(BUILD)/langevin_kernel.o $(BUILD)/jump_kernels.o $(BUILD)/text_kernels.o $(BUILD)/ranmar_abi.o
-HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh $(CSRC)/gauss_math.cuh
+HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh $(CSRC)/gauss_math.cuh $(CSRC)/crlog_table.inc
 
 .PHONY: all lib oracle ref clean sass
 all: lib oracle facade cexample cli
@@ -62,7 +62,25 @@ $(CLI): tools/ranmar_cli.cpp include/ranmar_b200.hpp $(LIB)
 	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../lib' -Wl,-rpath,/usr/local/cuda/lib64 -o $@
 
 # Microbenchmarks behind profiles/r1_micro.txt (run on a GPU box)
-MICRO := tools/micro/wbw tools/micro/ce tools/micro/pipes tools/micro/dtile
+MICRO := tools/micro/wbw tools/micro/ce tools/micro/pipes tools/micro/dtile tools/micro/intpipes
 micro: $(MICRO)
 tools/micro/%: tools/micro/%.cu
 	$(NVCC) -gencode arch=compute_100a,code=sm_100a -O3 -o $@ $<
+
+# The reference's own demos and acceptance suite compiled UNMODIFIED (in place
+# from /root/reference, never copied) against the drop-in headers
+# (include/ranmar/*.hpp -> ranmar_b200.hpp) and, for the expected output,
+# against the reference headers themselves. Outputs in tests/cpp/_ref/
+# (git-ignored; they travel to the GPU box with the snapshot).
+REFPROJ ?= /root/reference/proj
+DROPIN := tests/cpp/_ref
+dropin: $(LIB)
+	@test -d $(REFPROJ)/demo || (echo "reference sources not found at $(REFPROJ)"; exit 1)
+	@mkdir -p $(DROPIN)
+	for d in basic_usage parallel_streams; do \
+	  g++ -O2 -std=c++20 -Iinclude $(REFPROJ)/demo/$$d.cpp -L$(PKG)/lib -lranmar_b200 \
+	      -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib' -o $(DROPIN)/$$d || exit 1; \
+	  g++ -O2 -std=c++20 -Ioracle/shim -I$(REFPROJ)/include $(REFPROJ)/demo/$$d.cpp -o $(DROPIN)/$$d.ref || exit 1; \
+	done
+	g++ -O2 -std=c++20 -Iinclude -I$(REFPROJ)/tests $(REFPROJ)/tests/acceptance.cpp -L$(PKG)/lib -lranmar_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib' -o $(DROPIN)/acceptance

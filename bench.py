@@ -45,6 +45,25 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def measured_int_peaks():
+    """Integer-pipe peaks measured on a B200 of this pool by tools/micro/intpipes.cu
+    (raw JSON lines committed in profiles/r2_intpipes.txt): IMAD lane-ops/s (the
+    config-3 denominator) and the integer issue peak, the best of the IADD3/IMAD
+    mixes (the config-4 denominator). None if the file is missing."""
+    p = os.path.join(ROOT, "profiles", "r2_intpipes.txt")
+    if not os.path.exists(p):
+        return None
+    modes = {}
+    with open(p) as f:
+        for line in f:
+            if line.startswith("{"):
+                d = json.loads(line)
+                if "mode" in d:
+                    modes[d["mode"]] = d["lane_ops_per_s"]
+    issue = max(modes[k] for k in ("iadd", "mix_imad_iadd", "mix_imad_iadd_lop3"))
+    return {"imad": modes["imad"], "int_issue": issue, "source": "profiles/r2_intpipes.txt"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -104,11 +123,33 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup(gpus: int):
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` with N > 1 and no torchrun environment: re-run
+    this script under torch.distributed.run with one rank per GPU (the form the
+    driver uses), so the N-GPU number is never a 1-GPU run. Returns the exit
+    code, or None when this process is already a rank (or N = 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(gpus: int, need_gpu: bool):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world} ranks were launched")
+    if need_gpu and torch.cuda.device_count() < local + 1:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} CUDA device(s) visible")
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -148,37 +189,71 @@ def load_traffic(kernel_key: str):
 
 # ------------------------------------------------------------------ CPU arms
 
-def cpu_reference_c2(steps: int = 1, threads: int | None = None):
+def cpu_reference_c2(steps: int = 1, warmup: int = 1, threads: int | None = None,
+                     n: int | None = None):
     """The reference's own code (oracle/_ref, headers compiled in place) on the
-    host cores, on a bounded sample of config 2. Returns a dict or None."""
+    host cores: config 2's make_streams + step -> fp32 for n streams (default
+    all 65,536: the whole config, ~1 s per step on 16 cores), stored to host RAM.
+    Returns a dict, or None."""
     from oracle.bind import Reference, reference_available
     threads = threads or os.cpu_count() or 1
-    n = int(min(C2["n"], 16384, 1024 * threads))
-    out = np.empty(n * C2["per"], np.float32)
+    n = C2["n"] if n is None else n
+    per = C2["per"]
     if reference_available():
+        import psutil
         ref, kind = Reference(), "reference"
         base = ref.init(C2["seed"])
-        run = lambda: ref.generate_f32(base, C2["j"], 0, n, C2["per"], threads, out)  # noqa: E731
+        # the whole 16 GiB output when the host has room, else the same streams in
+        # passes over a 4 GiB buffer (identical work: every uniform is stored once)
+        chunk = n if psutil.virtual_memory().available > n * per * 4 + (8 << 30) else min(n, 16384)
+        out = np.empty(chunk * per, np.float32)
+
+        def run():
+            for lo in range(0, n, chunk):
+                ref.generate_f32(base, C2["j"], lo, min(chunk, n - lo), per, threads, out)
     else:  # fall back to the C restatement (single-threaded port)
         from oracle.bind import Oracle
-        orc, kind, threads = Oracle(), "port", 1
-        n = 256
-        out = np.empty(n * C2["per"], np.float32)
+        orc, kind, threads, chunk = Oracle(), "port", 1, 256
+        n = min(n, 256)
+        out = np.empty(n * per, np.float32)
 
         def run():
             ss = orc.make_streams(orc.init(C2["seed"]), C2["j"], n)
-            out[:] = orc.generate_f32(ss, C2["per"])
-    run()  # warm-up (page-faults the output buffer)
+            out[:] = orc.generate_f32(ss, per)
+    for _ in range(max(1, warmup)):
+        run()  # warm-up (page-faults the output buffer)
     times = []
     for _ in range(max(1, steps)):
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return {"value": n * C2["per"] / t, "unit": "uniforms/s", "cores": threads, "kind": kind,
-            "sample": f"config 2 streams [0, {n}) x {C2['per']} fp32 (make_streams + step, "
-                      f"stored to host RAM), {threads} threads, median of {len(times)}",
-            "seconds": t}
+    t = statistics.mean(times)
+    return {"value": n * per / t, "unit": "uniforms/s", "cores": threads, "kind": kind,
+            "sample": f"config 2 streams [0, {n}) x {per} fp32 (make_streams + next_f64, "
+                      f"stored to host RAM{'' if chunk == n else f' in passes of {chunk} streams'}), "
+                      f"{threads} threads, mean of {len(times)} steps",
+            "streams": n, "seconds": t, "steps": len(times)}
+
+
+def cpu_reference_c1():
+    """Config 1 on the reference's own single-thread loops (the CLI bench,
+    ranmar_cli.cpp:195-212): 10^8 x step() and 10^8 x step_float() from seed 12345."""
+    from oracle.bind import Reference, reference_available
+    if not reference_available():
+        return None
+    ref = Reference()
+    n = 10**8
+    s = ref.init(12345)
+    t0 = time.perf_counter()
+    ref.lib.ref_step_n(s.ctypes.data, n, None)
+    t1 = time.perf_counter()
+    fbuf = np.empty(n, np.float64)
+    t2 = time.perf_counter()
+    ref.lib.ref_step_float_n(12345, n, fbuf.ctypes.data)
+    t3 = time.perf_counter()
+    return {"workload": "one stream, seed 12345, 10^8 outputs, 1 thread",
+            "step_per_s": n / (t1 - t0), "step_float_per_s": n / (t3 - t2),
+            "step_ms": (t1 - t0) * 1e3, "step_float_ms": (t3 - t2) * 1e3, "cores": 1}
 
 
 def cpu_reference_text(states: np.ndarray):
@@ -252,16 +327,23 @@ def cpu_reference_extras():
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    cb = cpu_reference_c2(steps=args.steps)
+    # config 2 in full (65,536 streams = one rank's job), exactly --steps timed steps
+    cb = cpu_reference_c2(steps=args.steps, warmup=args.warmup)
     line = {"metric": METRIC, "impl": "reference", "value": cb["value"], "unit": "uniforms/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": cb["steps"], "warmup": args.warmup,
             "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, BASELINE config 2)",
-            "config": {"workload": "config 2 sample: make_streams(12345, 2^40) x 65536 fp32 per stream",
-                       "streams": cb["sample"]},
+            "config": {"workload": "config 2: make_streams(12345, 2^40) streams [0, 65536) x 65536 fp32 "
+                                   "uniforms stored" + ("" if world == 1 else
+                                                        f" (rank 0's share of the {world}-GPU job)"),
+                       "streams": cb["streams"], "per_stream": C2["per"],
+                       "same_config": cb["streams"] == C2["n"] and cb["kind"] == "reference"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "uniforms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    c1 = cpu_reference_c1()
+    if c1:
+        line["config1"] = c1
     extras = cpu_reference_extras()
     if extras:
         line.update(extras)
@@ -423,13 +505,16 @@ def run_ours(args, rank, world, local):
             "workload": "make_streams(init_unchecked(987654321), 2^120): 2^20 stream starts s_{kJ} per rank",
             "jump_aheads_per_s": n3 * world / (ms3 * 1e-3), "ms": ms3,
             "batched_jump_state_per_s": n3 * world / (msj * 1e-3), "batched_jump_ms": msj,
-            "macs_per_start_bulk": 97 * 97,
-            # whole config 3 (all launches) against the IMAD pipe at the rated SM clock
-            # (64 IMAD lanes/clk/SM x 148 SMs); the bulk kernel alone is in profiles/
-            "roofline": {"bound": "imad", "unit": "TMAC/s",
-                         "achieved": n3 * 97 * 97 / (ms3 * 1e-3) / 1e12,
-                         "peak": 64 * 148 * 1.965e9 / 1e12,
-                         "frac": n3 * 97 * 97 / (ms3 * 1e-3) / (64 * 148 * 1.965e9)}}
+            "macs_per_start_bulk": 97 * 97}
+        ip = measured_int_peaks()
+        if ip:
+            # whole config 3 (all launches) against the measured IMAD rate; the bulk
+            # kernel alone is in profiles/ (ncu)
+            ach = n3 * 97 * 97 / (ms3 * 1e-3)
+            extras["config3"]["roofline"] = {
+                "bound": "imad", "unit": "TMAC/s", "achieved": ach / 1e12, "peak": ip["imad"] / 1e12,
+                "frac": ach / ip["imad"], "peak_kind": f"measured ({ip['source']}, mode imad)",
+                "algorithmic_per_unit": "97 x 97 = 9,409 24-bit MACs per stream start"}
         # §8f row 1: export / re-import the 2^20 starts as reference text on the device
         text, off = rb.to_text_dev(st3, stream=stream)
         back, err = rb.from_text_dev(text, off, stream=stream)
@@ -482,6 +567,15 @@ def run_ours(args, rank, world, local):
         extras["config4"] = {"workload": f"{n4} streams x 2^20 uniforms consumed per rank "
                                          "(make_streams(42, 2^64) + per-stream u64 sum + 256-bin hist)",
                              "uniforms_per_s": n4 * C4["per"] * world / (ms4 * 1e-3), "ms": ms4}
+        ip = measured_int_peaks()
+        if ip:
+            # 9 int32 ops per uniform (core.hpp:56-65's 7 + sum + histogram)
+            ach = 9 * n4 * C4["per"] / (ms4 * 1e-3)
+            extras["config4"]["roofline"] = {
+                "bound": "int_issue", "unit": "Tops/s", "achieved": ach / 1e12,
+                "peak": ip["int_issue"] / 1e12, "frac": ach / ip["int_issue"],
+                "peak_kind": f"measured ({ip['source']}, best IADD3/IMAD mix)",
+                "algorithmic_per_unit": "9 int32 ops per uniform (SURVEY §8d C4)"}
         # after timing: all-gather the per-stream sums, all-reduce the histogram
         from paper_2512_00093_b200.shard import allgather_tensor, allreduce_sum
         all_sums = allgather_tensor(sums4)
@@ -583,7 +677,9 @@ def run_ours(args, rank, world, local):
         return
     cpu = None
     if world == 1 and not args.no_cpu:
-        cb = cpu_reference_c2(steps=1)
+        # a bounded sample (a quarter of config 2's streams, ~0.3 s on 16 cores):
+        # the full config is the reference arm's job (bench.py --impl reference)
+        cb = cpu_reference_c2(steps=1, warmup=1, n=16384)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     line = {
         "metric": METRIC, "value": value, "unit": "uniforms/s", "n_gpus": world,
@@ -618,7 +714,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--c4-streams", type=int, default=0)
     args = ap.parse_args()
-    rank, world, local = dist_setup(args.gpus)
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    rank, world, local = dist_setup(args.gpus, need_gpu=args.impl == "ours")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
     else:

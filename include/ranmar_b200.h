@@ -10,9 +10,12 @@
  *    gives a thread-local message. RANMAR_EINVAL is returned exactly where
  *    the reference throws std::invalid_argument (SURVEY §8b "Errors").
  *  - "_dev" functions take device pointers and a cudaStream_t passed as
- *    void*; they are asynchronous and stream-ordered, allocate nothing, and
- *    run hand-written sm_100a kernels. There is no CPU fallback: without a
- *    usable CUDA device they return RANMAR_ECUDA.
+ *    void*; they run on the CURRENT device (cudaSetDevice), are asynchronous
+ *    and stream-ordered, never allocate, never synchronise and never read
+ *    device memory back to the host, so a sequence of them can be captured
+ *    in a CUDA graph. They need the device's one-time resources from
+ *    ranmar_device_setup(device, stream) (else RANMAR_ESTATE). There is no
+ *    CPU fallback: without a usable CUDA device they return RANMAR_ECUDA.
  *  - "ranmar_ctx_*" functions take HOST buffers and do the host<->device
  *    copies themselves (pinned/pageable both accepted), synchronously.
  *  - Stream-major output layout: out[k * per_stream + n] is output n (0-based)
@@ -28,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RANMAR_ABI_VERSION 1
+#define RANMAR_ABI_VERSION 2
 
 enum {
     RANMAR_OK = 0,
@@ -100,6 +103,13 @@ int ranmar_from_text(const char* text, ranmar_state* out);
 
 /* -------------------------------------------------- device ops (async) --- */
 
+/* One-time, per-device setup for the _dev entry points (allocates and
+ * synchronises; idempotent, thread-safe): the sticky status word and the
+ * table of t^(2^k) mod the characteristic polynomial that every jump uses
+ * (the squarings of polyring.hpp:113-124, ~0.3 ms). `stream` belongs to
+ * `device`; the caller's current device is restored. ranmar_ctx_create calls it. */
+int ranmar_device_setup(int device, void* stream);
+
 /* Workspace bytes needed by ranmar_make_streams_dev / ranmar_jump_dev for n
  * streams. */
 size_t ranmar_make_streams_workspace(uint64_t n);
@@ -113,6 +123,12 @@ size_t ranmar_make_streams_workspace(uint64_t n);
 int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j, uint64_t first,
                             uint64_t n, ranmar_state* d_out, void* d_workspace,
                             size_t workspace_bytes, void* stream);
+
+/* The same with the base state in DEVICE memory (d_base). An invalid base
+ * raises the status bit (ranmar_device_status) instead of RANMAR_ESTATE. */
+int ranmar_make_streams_from_dev(const ranmar_state* d_base, const ranmar_jump_count* j,
+                                 uint64_t first, uint64_t n, ranmar_state* d_out,
+                                 void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* d_out[k] = ranmar::jump_state(d_in[k], J) for k < n (jump.hpp:90-95).
  * d_in == d_out is allowed. */
@@ -145,7 +161,7 @@ int ranmar_generate_float_dev(ranmar_float_state* d_states, uint64_t n_streams,
  * outputs land in order in d_out[0 .. count), and *d_state (device) ends
  * exactly as `count` calls of step() leave it (same ring layout). d_ws:
  * ranmar_generate_single_workspace(count) bytes (0 for count <= 8192). The
- * state is read back to the host once (synchronises the stream). */
+ * state stays on the device (an invalid one raises the status bit). */
 size_t ranmar_generate_single_workspace(uint64_t count);
 int ranmar_generate_single_u32_dev(ranmar_state* d_state, uint64_t count, uint32_t* d_out,
                                    void* d_ws, size_t ws_bytes, void* stream);
@@ -207,6 +223,15 @@ int ranmar_langevin_bank_dev(uint32_t* d_bank, uint64_t n_atoms, uint64_t t, con
 int ranmar_fp64_selfcheck_dev(uint64_t n, uint64_t seed, unsigned long long* d_mismatches,
                               void* stream);
 
+/* Diagnostic: exhaustive check of gaussian()'s correctly rounded log on
+ * rsq = s / 2^46, s in [s0, s0 + n) (the whole domain is s in [1, 2^46)).
+ * Adds to d_counts[0..3]: inputs the fast phase could not decide, inputs the
+ * accurate phase could not decide either, (mode 1) fast/accurate disagreements,
+ * and the number of inputs recorded in d_fails[0 .. cap) (no particular order):
+ * the fast-phase failures (modes 0, 1) or the accurate-phase failures (mode 2). */
+int ranmar_crlog_sweep_dev(uint64_t s0, uint64_t n, int32_t mode, unsigned long long* d_counts,
+                           uint64_t* d_fails, uint64_t cap, void* stream);
+
 /* The same gaussian() calls for FEW streams with MANY calls each: one warp per
  * stream (serves the scalar RanMars-style facade). d_out[s * count + q] is
  * call q of stream s. States and cached deviates advance in place. */
@@ -237,6 +262,28 @@ int ranmar_device_status(uint32_t* flags, int clear);
  * diagnostic evidence for benchmarks ("gpu_launches"). */
 uint64_t ranmar_kernel_launches(void);
 
+/* Per-step trace for the scalar step()/next_f64() of the C++ facade: for
+ * step n of stream k, at index k * per_stream + n: d_u = the output
+ * (core.hpp:65), d_x = the word step() writes into lane[i] (core.hpp:56-57),
+ * d_v = the residue after the step (core.hpp:61-63). States advance in place. */
+int ranmar_generate_trace_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                              uint32_t* d_u, uint32_t* d_x, uint32_t* d_v, void* stream);
+/* The same for reference::step_float (float_ranmar.hpp:33-46): outputs, the
+ * values written into x[i] and the new c. */
+int ranmar_generate_float_trace_dev(ranmar_float_state* d_states, uint64_t n_streams,
+                                    uint64_t per_stream, double* d_out, double* d_y, double* d_c,
+                                    void* stream);
+/* ranmar::poly on the device: d_out[q] = d_a[q] * d_b[q] mod phi (mul_mod,
+ * polyring.hpp:85-98) for q < n (97 words each), and d_out[q] = d_raw[q] mod
+ * phi (reduce_trinomial, polyring.hpp:60-80; 193 raw words each). */
+int ranmar_poly_mul_mod_dev(const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n,
+                            void* stream);
+int ranmar_poly_reduce_dev(const uint32_t* d_raw, uint32_t* d_out, uint64_t n, void* stream);
+
+/* The calling thread's current CUDA device (cudaGetDevice), for callers that
+ * do not include the CUDA runtime headers. */
+int ranmar_current_device(int* device);
+
 /* ------------------------------------------- host-buffer ops (sync, e2e) --- */
 int ranmar_ctx_create(int device, ranmar_ctx** out);
 void ranmar_ctx_destroy(ranmar_ctx* ctx);
@@ -260,6 +307,30 @@ int ranmar_ctx_gaussian_stream(ranmar_ctx* ctx, ranmar_gauss_state* h_g, uint64_
                                uint64_t count, double* h_out);
 /* Bytes moved host->device and device->host by the last ctx call. */
 int ranmar_ctx_last_traffic(ranmar_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+/* Host-buffer forms of the trace, pow_t_mod and poly primitives (the C++
+ * facade's step(), reference::step_float(), poly::pow_t_mod / mul_mod /
+ * reduce_trinomial). */
+int ranmar_ctx_generate_trace(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n,
+                              uint64_t per_stream, uint32_t* h_u, uint32_t* h_x, uint32_t* h_v);
+int ranmar_ctx_float_trace(ranmar_ctx* ctx, ranmar_float_state* h_states, uint64_t n,
+                           uint64_t per_stream, double* h_out, double* h_y, double* h_c);
+int ranmar_ctx_pow_t_mod(ranmar_ctx* ctx, const ranmar_jump_count* j, uint32_t* h_coeff);
+int ranmar_ctx_poly_mul_mod(ranmar_ctx* ctx, const uint32_t* h_a, const uint32_t* h_b,
+                            uint32_t* h_out, uint64_t n);
+int ranmar_ctx_poly_reduce(ranmar_ctx* ctx, const uint32_t* h_raw, uint32_t* h_out, uint64_t n);
+
+/* Host-buffer forms of the trace, pow_t_mod and poly primitives (the C++
+ * facade's step(), reference::step_float(), poly::pow_t_mod / mul_mod /
+ * reduce_trinomial). */
+int ranmar_ctx_generate_trace(ranmar_ctx* ctx, ranmar_state* h_states, uint64_t n,
+                              uint64_t per_stream, uint32_t* h_u, uint32_t* h_x, uint32_t* h_v);
+int ranmar_ctx_float_trace(ranmar_ctx* ctx, ranmar_float_state* h_states, uint64_t n,
+                           uint64_t per_stream, double* h_out, double* h_y, double* h_c);
+int ranmar_ctx_pow_t_mod(ranmar_ctx* ctx, const ranmar_jump_count* j, uint32_t* h_coeff);
+int ranmar_ctx_poly_mul_mod(ranmar_ctx* ctx, const uint32_t* h_a, const uint32_t* h_b,
+                            uint32_t* h_out, uint64_t n);
+int ranmar_ctx_poly_reduce(ranmar_ctx* ctx, const uint32_t* h_raw, uint32_t* h_out, uint64_t n);
 
 #ifdef __cplusplus
 }

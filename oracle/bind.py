@@ -81,7 +81,11 @@ class Oracle:
             "or_generate_f32": (None, [vp, u64, u64, vp]),
             "or_consume": (None, [vp, u64, u64, vp, vp]),
             "or_gaussian_fill": (None, [vp, u64, u64, u64, vp]),
-            "or_glog": (C.c_double, [C.c_double]),
+            "or_gaussian_fill_flags": (None, [vp, u64, u64, u64, vp, vp]),
+            "or_crlog": (C.c_double, [C.c_double]),
+            "or_crlog_ex": (C.c_double, [C.c_double, C.POINTER(C.c_int)]),
+            "or_crlog_accurate": (C.c_double, [C.c_double, C.POINTER(C.c_int)]),
+            "or_crlog_scan": (u64, [u64, u64, vp, u64]),
             "or_langevin": (i32, [vp, u64, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32,
                                   C.c_double, C.c_int]),
             "or_gaussian": (C.c_double, [vp]),
@@ -184,18 +188,23 @@ class Oracle:
         return sums, hist
 
     def gaussian_fill(self, gstates: np.ndarray, per_step: int, steps: int,
-                      libm_log: bool = False) -> np.ndarray:
-        """The repo's gaussian() convention; libm_log=True swaps in glibc log()
-        (diagnostic only: how far the convention's log is from the platform's)."""
+                      libm_log: bool = False, with_flags: bool = False):
+        """The repo's gaussian() (RanMars::gaussian's form, correctly rounded
+        log); libm_log=True swaps in glibc log() (the same form with the
+        platform's libm, which is not correctly rounded on ~0.08 % of inputs).
+        with_flags: also return, per deviate, whether its pair's glibc log
+        differed from the correctly rounded one (libm mode)."""
         gstates = np.ascontiguousarray(gstates)
         out = np.empty((steps, len(gstates), per_step), np.float64)
+        flags = np.zeros(out.shape, np.uint8) if with_flags else None
         flag = C.c_int.in_dll(self.lib, "or_gauss_use_libm_log")
         flag.value = int(libm_log)
         try:
-            self.lib.or_gaussian_fill(_p(gstates), len(gstates), per_step, steps, _p(out))
+            self.lib.or_gaussian_fill_flags(_p(gstates), len(gstates), per_step, steps, _p(out),
+                                            None if flags is None else _p(flags))
         finally:
             flag.value = 0
-        return out
+        return (out, flags) if with_flags else out
 
     def langevin(self, gstates: np.ndarray, v: np.ndarray, f: np.ndarray, types: np.ndarray,
                  gfactor1: np.ndarray, gfactor2: np.ndarray, tsqrt: float, noise: int,
@@ -209,8 +218,28 @@ class Oracle:
                                     None if mask is None else _p(mask), groupbit, _p(gfactor1),
                                     _p(gfactor2), len(gfactor1) - 1, tsqrt, noise)
 
-    def glog(self, x: float) -> float:
-        return self.lib.or_glog(x)
+    def crlog(self, x: float) -> float:
+        """gaussian()'s correctly rounded log."""
+        return self.lib.or_crlog(x)
+
+    def crlog_ex(self, x: float):
+        """(log, decided by the fast phase?)"""
+        f = C.c_int()
+        y = self.lib.or_crlog_ex(x, C.byref(f))
+        return y, bool(f.value)
+
+    def crlog_accurate(self, x: float):
+        """(accurate phase's log, its rounding test decided?)"""
+        ok = C.c_int()
+        y = self.lib.or_crlog_accurate(x, C.byref(ok))
+        return y, bool(ok.value)
+
+    def crlog_scan(self, s0: int, n: int, cap: int = 1 << 16):
+        """Fast-phase failures over rsq = s / 2^46, s in [s0, s0 + n):
+        (count, the first <= cap failing s values)."""
+        fails = np.zeros(max(cap, 1), np.uint64)
+        c = self.lib.or_crlog_scan(s0, n, _p(fails), cap)
+        return int(c), fails[: min(c, cap)].tolist()
 
     def gaussian_call(self, g: np.ndarray) -> float:
         """One gaussian() call on a 1-element GAUSS_DTYPE array (advanced in place)."""

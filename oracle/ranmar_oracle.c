@@ -370,51 +370,197 @@ void or_consume(or_state* states, uint64_t n_streams, uint64_t per_stream, uint6
     }
 }
 
-/* The gaussian convention's log(): a fixed sequence of IEEE operations
- * (binary64 +, -, *, / and fused multiply-add, each correctly rounded) so the
- * device can reproduce it bit for bit. x = 2^k m with m in (sqrt2/2, sqrt2],
- * f = m - 1 (exact), s = f / (2 + f), log1p(f) = 2 atanh(s) with the Taylor
- * series of atanh to s^21 (|s| <= 0.1716, truncation < 2^-60 relative), and
- * k ln2 added as a 42-bit head (exact k * head) plus a tail. Accuracy ~1 ulp
- * (the rounding of s dominates); x must be a positive normal double, which
- * rsq in (0, 1) of the polar method always is (rsq >= 2^-46). */
-double or_glog(double x) {
+/* The gaussian convention's log(): CORRECTLY ROUNDED binary64 log, so the
+ * repo's gaussian() equals LAMMPS' RanMars::gaussian() form
+ * fac = sqrt(-2.0*log(rsq)/rsq) with any correctly rounded libm log (glibc's
+ * log is correctly rounded except in rare cases, where it is 1 ulp off). The
+ * method restates the published two-phase scheme of CRlibm / CORE-MATH
+ * (Ziv's strategy): a fast double-double evaluation with a rigorous error
+ * bound and a rounding test, and an accurate path (~2^-103) for the rare
+ * inputs whose log lies too close to a rounding boundary. The constants come
+ * from tools/gen_crlog.py (crlog_table.inc, the same file as the device's);
+ * every operation below is one IEEE binary64 operation (-ffp-contract=off;
+ * fma() is the correctly rounded fused multiply-add), so the device
+ * (csrc/gauss_math.cuh crlog) reproduces each step bit for bit.
+ *
+ *   x = 2^e m, m in [1,2), i = top 7 bits of m, h = (i >= CRLOG_SPLIT)
+ *   z = m r_i - 1                        exact (|z| < 2^-7, r_i = R_i/256)
+ *   log x = (e+h) ln2 + T_i + log1p(z)   T_i = -log(r_i 2^h) (table)
+ *
+ * Fast-path error (absolute, derived in DESIGN.md §5.2):
+ *   |log x - (yh + yl)| <= 2^-49 |z^3| + 2^-88 |yh|;
+ * the test accepts yh when yh + (yl +- bound) round to the same double.
+ * x must be a positive normal double: gaussian()'s rsq is in [2^-46, 1). */
+#define CRLOG_TABLE_QUAL static const
+#include "crlog_table.inc"
+
+static void or_two_sum(double a, double b, double* s, double* e) {
+    const double t = a + b;
+    const double bb = t - a;
+    *e = (a - (t - bb)) + (b - bb);
+    *s = t;
+}
+
+/* the argument reduction shared by both phases */
+static void or_crlog_reduce(double x, int* i, double* ed, double* z) {
     uint64_t b;
     memcpy(&b, &x, 8);
-    int k = (int)((b >> 52) & 0x7FF) - 1023;
+    *i = (int)((b >> 45) & 127);
+    *ed = (double)((int)(b >> 52) - 1023 + (*i >= CRLOG_SPLIT));
     const uint64_t mb = (b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
     double m;
     memcpy(&m, &mb, 8);
-    if (m > 0x1.6a09e667f3bcdp+0) { /* sqrt(2) */
-        m *= 0.5;
-        k += 1;
-    }
-    const double f = m - 1.0;
-    const double s = f / (2.0 + f);
-    const double z = s * s;
-    double p = 0x1.8618618618618p-5;     /* 1/21 */
-    p = fma(p, z, 0x1.af286bca1af28p-5); /* 1/19 */
-    p = fma(p, z, 0x1.e1e1e1e1e1e1ep-5); /* 1/17 */
-    p = fma(p, z, 0x1.1111111111111p-4); /* 1/15 */
-    p = fma(p, z, 0x1.3b13b13b13b14p-4); /* 1/13 */
-    p = fma(p, z, 0x1.745d1745d1746p-4); /* 1/11 */
-    p = fma(p, z, 0x1.c71c71c71c71cp-4); /* 1/9 */
-    p = fma(p, z, 0x1.2492492492492p-3); /* 1/7 */
-    p = fma(p, z, 0x1.999999999999ap-3); /* 1/5 */
-    p = fma(p, z, 0x1.5555555555555p-2); /* 1/3 */
-    const double t = s * z;
-    const double l1p = 2.0 * fma(t, p, s); /* 2 atanh(s) */
-    const double kd = (double)k;
-    return fma(kd, 0x1.62e42fefa3800p-1, fma(kd, 0x1.ef35793c76730p-45, l1p));
+    *z = fma(m, crlog_r[*i], -1.0);
 }
 
-int or_gauss_use_libm_log = 0; /* diagnostic: 1 = glibc log() instead of or_glog */
+/* Accurate phase: log1p(z) by its Taylor series to z^15 (truncation
+ * < 2^-109 relative), terms 8..15 in double, 7..1 in double-double Horner;
+ * (e+h) ln2 as an exact head, an exact double-double middle and a tail;
+ * T_i as three doubles; everything summed in double-double. *ok = 0 when the
+ * rounding test at 2^-98 fails too (never on the gaussian domain: the GPU
+ * sweep ranmar_crlog_sweep_dev checks all 2^46 inputs, and the few it finds
+ * undecided are tabulated with their correctly rounded logs, crlog_hard). */
+double or_crlog_accurate(double x, int* ok) {
+    int i;
+    double ed, z;
+    or_crlog_reduce(x, &i, &ed, &z);
+    double p = CRLOG_A15;
+    p = fma(p, z, CRLOG_A14);
+    p = fma(p, z, CRLOG_A13);
+    p = fma(p, z, CRLOG_A12);
+    p = fma(p, z, CRLOG_A11);
+    p = fma(p, z, CRLOG_A10);
+    p = fma(p, z, CRLOG_A9);
+    p = fma(p, z, CRLOG_A8);
+    static const double ch[8] = {0, 1.0, -0.5, CRLOG_A3H, CRLOG_A4H, CRLOG_A5H, CRLOG_A6H, CRLOG_A7H};
+    static const double cl[8] = {0, 0.0, 0.0, CRLOG_A3L, CRLOG_A4L, CRLOG_A5L, CRLOG_A6L, CRLOG_A7L};
+    double ph = p, pl = 0.0;
+    for (int k = 7; k >= 1; --k) {
+        /* (ph, pl) = (ph, pl) * z + c_k */
+        const double th = ph * z;
+        const double tl = fma(pl, z, fma(ph, z, -th));
+        double s, e;
+        or_two_sum(th, ch[k], &s, &e);
+        e = e + (tl + cl[k]);
+        ph = s + e;
+        pl = e - (ph - s);
+    }
+    {   /* log1p(z) = (ph, pl) * z */
+        const double th = ph * z;
+        const double tl = fma(pl, z, fma(ph, z, -th));
+        ph = th + tl;
+        pl = tl - (ph - th);
+    }
+    /* K + T: head e ln2_hi + t1 (Fast2Sum: |e ln2_hi| >= |t1| or e = 0) */
+    const double k1 = ed * CRLOG_LN2_HI;
+    const double t1 = crlog_t12[2 * i], t2 = crlog_t12[2 * i + 1], t3 = crlog_t3[i];
+    double hi = k1 + t1;
+    double lo = t1 - (hi - k1);
+    const double k2h = ed * CRLOG_LN2_MID;
+    const double k2l = fma(ed, CRLOG_LN2_MID, -k2h);
+    const double small = (k2l + t3) + ed * CRLOG_LN2_LO;
+    double s, e;
+    /* + k2h */
+    or_two_sum(hi, k2h, &s, &e);
+    e = e + lo;
+    hi = s + e;
+    lo = e - (hi - s);
+    /* + t2 */
+    or_two_sum(hi, t2, &s, &e);
+    e = e + lo;
+    hi = s + e;
+    lo = e - (hi - s);
+    /* + log1p(z) */
+    or_two_sum(hi, ph, &s, &e);
+    e = e + ((lo + pl) + small);
+    hi = s + e;
+    lo = e - (hi - s);
+    const double d = fabs(hi) * 0x1p-98;
+    *ok = (hi + (lo + d)) == (hi + (lo - d));
+    if (!*ok) /* the few domain inputs that even this cannot decide are tabulated */
+        for (int k = 0; k < CRLOG_NHARD; ++k)
+            if (x == crlog_hard[2 * k]) {
+                *ok = 1;
+                return crlog_hard[2 * k + 1];
+            }
+    return hi;
+}
+
+/* Fast phase; *fast = 1 when its rounding test decided the result. */
+double or_crlog_ex(double x, int* fast) {
+    int i;
+    double ed, z;
+    or_crlog_reduce(x, &i, &ed, &z);
+    /* log1p(z) = z - z^2/2 + z^3 q(z), q = 1/3 - z/4 + ... - z^7/10 */
+    const double zh = z * z;
+    const double zl = fma(z, z, -zh);
+    double q = CRLOG_C10;
+    q = fma(q, z, CRLOG_C9);
+    q = fma(q, z, CRLOG_C8);
+    q = fma(q, z, CRLOG_C7);
+    q = fma(q, z, CRLOG_C6);
+    q = fma(q, z, CRLOG_C5);
+    q = fma(q, z, CRLOG_C4);
+    q = fma(q, z, CRLOG_C3);
+    const double z3 = z * zh;
+    const double hh = -0.5 * zh;            /* exact */
+    const double s1 = z + hh;               /* Fast2Sum: |z| >= |hh| */
+    const double e1 = hh - (s1 - z);
+    const double lo1 = fma(z3, q, e1 + (-0.5 * zl));
+    /* K + T_i: Fast2Sum (|e ln2_hi| >= |t1| unless e = 0) */
+    const double k1 = ed * CRLOG_LN2_HI;    /* exact: 42-bit head */
+    const double t1 = crlog_t12[2 * i], t2 = crlog_t12[2 * i + 1];
+    const double ah = k1 + t1;
+    const double al = t1 - (ah - k1);
+    /* + log1p head: TwoSum */
+    double bh, bl;
+    or_two_sum(ah, s1, &bh, &bl);
+    double lo = fma(ed, CRLOG_LN2_MID, t2) + al;
+    lo = lo + bl;
+    lo = lo + lo1;
+    const double yh = bh + lo;               /* Fast2Sum: |bh| >= |lo| */
+    const double yl = lo - (yh - bh);
+    const double d = fma(fabs(z3), 0x1p-49, fabs(yh) * 0x1p-88);
+    if ((yh + (yl + d)) == (yh + (yl - d))) {
+        *fast = 1;
+        return yh;
+    }
+    *fast = 0;
+    int ok;
+    return or_crlog_accurate(x, &ok);
+}
+
+double or_crlog(double x) {
+    int fast;
+    return or_crlog_ex(x, &fast);
+}
+
+/* Diagnostics for tests: over rsq = s / 2^46, s = s0 .. s0 + n - 1, the s
+ * whose fast phase fails (up to cap of them, returns the total count). */
+uint64_t or_crlog_scan(uint64_t s0, uint64_t n, uint64_t* fails, uint64_t cap) {
+    uint64_t c = 0;
+    for (uint64_t k = 0; k < n; ++k) {
+        const double x = (double)(s0 + k) * 0x1p-46;
+        int fast;
+        (void)or_crlog_ex(x, &fast);
+        if (!fast) {
+            if (c < cap) fails[c] = s0 + k;
+            ++c;
+        }
+    }
+    return c;
+}
+
+int or_gauss_use_libm_log = 0; /* diagnostic: 1 = glibc log() instead of or_crlog */
+/* set by or_gaussian for each NEW pair: glibc's log(rsq) != or_crlog(rsq) */
+int or_gauss_last_log_differs = 0;
 
 /* Repo-defined gaussian(): Marsaglia polar method on uniform() = next_f64
  * (core.hpp:70-72). Pair convention as in Numerical Recipes' gasdev: draw
  * v1 then v2 (each 2u-1), reject while rsq >= 1 or rsq == 0, return v2*fac
- * and cache v1*fac for the next call; log is or_glog above, every other
- * operation a single IEEE binary64 operation. NOT pinned to LAMMPS (absent). */
+ * and cache v1*fac for the next call (LAMMPS RanMars::gaussian's form); log
+ * is the correctly rounded or_crlog above, every other operation a single
+ * IEEE binary64 operation. */
 double or_gaussian(or_gauss_state* g) {
     if (g->has_saved) {
         g->has_saved = 0;
@@ -426,7 +572,8 @@ double or_gaussian(or_gauss_state* g) {
         v2 = 2.0 * ((double)or_step(&g->s) * 0x1p-24) - 1.0;
         rsq = v1 * v1 + v2 * v2;
     } while (rsq >= 1.0 || rsq == 0.0);
-    const double lg = or_gauss_use_libm_log ? log(rsq) : or_glog(rsq);
+    const double lg = or_gauss_use_libm_log ? log(rsq) : or_crlog(rsq);
+    or_gauss_last_log_differs = or_gauss_use_libm_log && lg != or_crlog(rsq);
     const double fac = sqrt(-2.0 * lg / rsq);
     g->saved = v1 * fac;
     g->has_saved = 1;
@@ -435,10 +582,27 @@ double or_gaussian(or_gauss_state* g) {
 
 void or_gaussian_fill(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step, uint64_t steps,
                       double* out) {
-    for (uint64_t a = 0; a < n_atoms; ++a)
+    or_gaussian_fill_flags(g, n_atoms, per_step, steps, out, NULL);
+}
+
+/* The same, and (libm mode) flags[idx] = 1 when deviate idx comes from a pair
+ * whose rsq has glibc log(rsq) != correctly rounded log(rsq). A deviate
+ * cached before the call counts as unflagged. */
+void or_gaussian_fill_flags(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step,
+                            uint64_t steps, double* out, uint8_t* flags) {
+    for (uint64_t a = 0; a < n_atoms; ++a) {
+        int pending = 0;
         for (uint64_t st = 0; st < steps; ++st)
-            for (uint64_t c = 0; c < per_step; ++c)
-                out[(st * n_atoms + a) * per_step + c] = or_gaussian(&g[a]);
+            for (uint64_t c = 0; c < per_step; ++c) {
+                const uint64_t idx = (st * n_atoms + a) * per_step + c;
+                const int cached = g[a].has_saved != 0;
+                out[idx] = or_gaussian(&g[a]);
+                if (flags) {
+                    flags[idx] = (uint8_t)(cached ? pending : or_gauss_last_log_differs);
+                    if (!cached) pending = or_gauss_last_log_differs;
+                }
+            }
+    }
 }
 
 /* Repo-defined fix-langevin-style consumer (no

@@ -102,7 +102,10 @@ typedef struct or_gauss_state {
     uint32_t has_saved;
     uint32_t pad;
 } or_gauss_state;
-double or_glog(double x);
+double or_crlog(double x);                    /* correctly rounded log, x > 0 normal */
+double or_crlog_ex(double x, int* fast);      /* *fast: the fast phase decided */
+double or_crlog_accurate(double x, int* ok);  /* accurate phase alone */
+uint64_t or_crlog_scan(uint64_t s0, uint64_t n, uint64_t* fails, uint64_t cap);
 extern int or_gauss_use_libm_log;
 double or_gaussian(or_gauss_state* g);
 /* Repo-defined fix-langevin-style consumer; returns 1 if an atom type was out
@@ -113,6 +116,8 @@ int or_langevin(or_gauss_state* g, uint64_t n_atoms, const double* v, double* f,
                 int noise);
 void or_gaussian_fill(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step, uint64_t steps,
                       double* out /* [step][atom][per_step] */);
+void or_gaussian_fill_flags(or_gauss_state* g, uint64_t n_atoms, uint64_t per_step,
+                            uint64_t steps, double* out, uint8_t* flags);
 
 /* Text state (serialize.hpp:21-136). */
 long or_to_text(const or_state* s, char* buf, long cap);

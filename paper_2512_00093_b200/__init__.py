@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import functools
 import os
 from typing import Optional, Tuple
 
@@ -77,7 +78,9 @@ def lib() -> C.CDLL:
         "ranmar_to_text": (C.c_long, [vp, C.c_char_p, C.c_long]),
         "ranmar_from_text": (i32, [C.c_char_p, vp]),
         "ranmar_make_streams_workspace": (sz, [u64]),
+        "ranmar_device_setup": (i32, [i32, vp]),
         "ranmar_make_streams_dev": (i32, [vp, jp, u64, u64, vp, vp, sz, vp]),
+        "ranmar_make_streams_from_dev": (i32, [vp, jp, u64, u64, vp, vp, sz, vp]),
         "ranmar_jump_dev": (i32, [vp, vp, u64, jp, vp, sz, vp]),
         "ranmar_pow_t_mod_dev": (i32, [jp, vp, vp]),
         "ranmar_generate_u32_dev": (i32, [vp, u64, u64, vp, vp]),
@@ -86,6 +89,7 @@ def lib() -> C.CDLL:
         "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
         "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
+        "ranmar_crlog_sweep_dev": (i32, [u64, u64, i32, vp, vp, u64, vp]),
         "ranmar_bank_words": (u64, [u64]),
         "ranmar_generate_single_workspace": (sz, [u64]),
         "ranmar_generate_single_u32_dev": (i32, [vp, u64, vp, vp, sz, vp]),
@@ -149,6 +153,53 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RanmarError("no CUDA device: the B200 kernels are the only implementation")
+    return torch
+
+
+def _dptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+_ready = set()
+
+
+def device_setup(device: Optional[int] = None) -> None:
+    """ranmar_device_setup: the one-time per-device resources of the _dev entry
+    points (status word, table of squares). Called automatically by every
+    device function below; call it yourself before capturing a CUDA graph."""
+    torch = _torch()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    if dev not in _ready:
+        with torch.cuda.device(dev):
+            s = torch.cuda.current_stream(dev)
+            _check(lib().ranmar_device_setup(dev, C.c_void_p(s.cuda_stream)))
+        _ready.add(dev)
+
+
+def _on_device(fn):
+    """Run a device function on the device of its first CUDA tensor argument (or
+    the current device), set up, and with that device current; the caller's
+    current device is restored afterwards (the C ABI works on the current device)."""
+    @functools.wraps(fn)
+    def wrap(*args, **kw):
+        torch = _torch()
+        dev = None
+        for a in (*args, *kw.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                dev = a.device.index
+                break
+        if dev is None:
+            dev = torch.cuda.current_device()
+        device_setup(dev)
+        with torch.cuda.device(dev):
+            return fn(*args, **kw)
+    return wrap
+
+
 # ----------------------------------------------------------------- host side
 
 def init(seed: int) -> np.ndarray:
@@ -176,6 +227,7 @@ def init_float(seed: int) -> np.ndarray:
     return f
 
 
+@_on_device
 def generate_float(fstates, per_stream: int, out=None, stream=None):
     """per_stream calls of reference::step_float (Algorithm 1, binary64) per float
     state (uint8 CUDA tensor [n, 792]), advanced in place -> float64 [n * per_stream]."""
@@ -228,13 +280,6 @@ def from_text(text: str) -> np.ndarray:
 
 # ---------------------------------------------------------------- device side
 
-def _torch():
-    import torch
-    if not torch.cuda.is_available():
-        raise RanmarError("no CUDA device: the B200 kernels are the only implementation")
-    return torch
-
-
 def _stream_ptr(stream) -> C.c_void_p:
     torch = _torch()
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -253,10 +298,7 @@ def states_to_host(t) -> np.ndarray:
     return t.detach().cpu().contiguous().numpy().view(STATE_DTYPE).reshape(-1)
 
 
-def _dptr(t) -> C.c_void_p:
-    return C.c_void_p(t.data_ptr())
-
-
+@_on_device
 def make_streams_dev(base: np.ndarray, j, n: int, first: int = 0, out=None, workspace=None,
                      stream=None):
     """Streams [first, first+n) of make_streams(base, J) (jump.hpp:108-124) on the GPU.
@@ -276,6 +318,7 @@ def make_streams_dev(base: np.ndarray, j, n: int, first: int = 0, out=None, work
     return out
 
 
+@_on_device
 def make_streams(seed: int, block_length, n_streams: int,
                  mode: StreamMode = StreamMode.incremental, first: int = 0):
     """ranmar::make_streams(seed, J, n, mode) (jump.hpp:108-124), computed on the GPU.
@@ -287,6 +330,7 @@ def make_streams(seed: int, block_length, n_streams: int,
     return make_streams_dev(init(seed), block_length, n_streams, first=first)
 
 
+@_on_device
 def jump_dev(states, j, out=None, stream=None):
     """out[k] = jump_state(states[k], J) (jump.hpp:90-95)."""
     torch = _torch()
@@ -305,6 +349,7 @@ def jump_state(state: np.ndarray, j) -> np.ndarray:
     return states_to_host(jump_dev(states_to_device(state), j))
 
 
+@_on_device
 def pow_t_mod_dev(j, stream=None):
     """ranmar::poly::pow_t_mod<24>(J) (polyring.hpp:113-124) -> int32 CUDA tensor [97]."""
     torch = _torch()
@@ -318,6 +363,7 @@ _GEN = {"u32": ("ranmar_generate_u32_dev", "int32"), "f32": ("ranmar_generate_f3
         "f64": ("ranmar_generate_f64_dev", "float64")}
 
 
+@_on_device
 def generate(states, per_stream: int, fmt: str = "f32", out=None, stream=None):
     """per_stream x step() per stream (core.hpp:54-72), states advanced in place.
     Returns the stream-major output [n * per_stream] (u32 outputs as int32)."""
@@ -330,6 +376,7 @@ def generate(states, per_stream: int, fmt: str = "f32", out=None, stream=None):
     return out
 
 
+@_on_device
 def consume(states, per_stream: int, sums=None, hist=None, stream=None):
     """Per-stream u64 sum of the 24-bit outputs and 256-bin histogram of u >> 16."""
     torch = _torch()
@@ -343,6 +390,7 @@ def consume(states, per_stream: int, sums=None, hist=None, stream=None):
     return sums, hist
 
 
+@_on_device
 def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
     """steps x per_step gaussian() calls per atom -> out[step, atom, c] (float64)."""
     torch = _torch()
@@ -371,6 +419,7 @@ def langevin_factors(mass, t_period: float, dt: float, noise: int = NOISE_UNIFOR
     return np.ascontiguousarray(g1), np.ascontiguousarray(g2)
 
 
+@_on_device
 def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int = NOISE_UNIFORM,
              mask=None, groupbit: int = 1, stream=None):
     """Fix-langevin-style consumer on CUDA tensors: for atoms in the group,
@@ -392,6 +441,7 @@ def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int 
     return f
 
 
+@_on_device
 def generate_single(state, count: int, fmt: str = "f32", out=None, stream=None):
     """count outputs of ONE stream (a [1, 100] CUDA state tensor, advanced in place
     exactly as count calls of step()) computed as 8,192-output substreams."""
@@ -407,6 +457,7 @@ def generate_single(state, count: int, fmt: str = "f32", out=None, stream=None):
     return out
 
 
+@_on_device
 def bank_from_states(states, stream=None):
     """[n, 100] (or gauss [n, 104]) state tensor -> stream bank [99, n] (int32 words)."""
     torch = _torch()
@@ -417,6 +468,7 @@ def bank_from_states(states, stream=None):
     return bank
 
 
+@_on_device
 def bank_to_states(bank, t: int, out=None, stream=None):
     """Stream bank at t outputs per stream -> [n, 100] states (as t calls of step())."""
     torch = _torch()
@@ -427,6 +479,7 @@ def bank_to_states(bank, t: int, out=None, stream=None):
     return out
 
 
+@_on_device
 def langevin_bank(bank, t: int, v, f, types, gfactor1, gfactor2, tsqrt: float, stream=None) -> int:
     """Uniform-noise Langevin on a stream bank (every atom draws 3); returns t + 3."""
     n = bank.shape[1]
@@ -438,6 +491,7 @@ def langevin_bank(bank, t: int, v, f, types, gfactor1, gfactor2, tsqrt: float, s
     return t + 3
 
 
+@_on_device
 def fp64_selfcheck(n: int, seed: int = 1) -> int:
     """Bitwise mismatches between gaussian()'s branch-free fp64 divide/sqrt and
     the CUDA library's correctly rounded ones over n operand sets (expected 0)."""
@@ -447,6 +501,20 @@ def fp64_selfcheck(n: int, seed: int = 1) -> int:
     return int(bad.item())
 
 
+@_on_device
+def crlog_sweep(s0: int, n: int, mode: int = 0, cap: int = 1 << 16):
+    """Check gaussian()'s correctly rounded log on rsq = s / 2^46, s in
+    [s0, s0 + n): returns (fast-phase failures, accurate-phase failures,
+    fast/accurate disagreements (mode 1), the failing s values (<= cap))."""
+    torch = _torch()
+    counts = torch.zeros(4, dtype=torch.int64, device="cuda")
+    fails = torch.zeros(max(cap, 1), dtype=torch.int64, device="cuda")
+    _check(lib().ranmar_crlog_sweep_dev(s0, n, mode, _dptr(counts), _dptr(fails), cap, None))
+    c = counts.cpu().tolist()
+    return c[0], c[1], c[2], sorted(fails[: min(c[3], cap)].cpu().tolist())
+
+
+@_on_device
 def gaussian_stream(gstates, count: int, out=None, stream=None):
     """count gaussian() calls on each of a FEW streams (one warp per stream) ->
     out[stream, q] (float64); states and cached deviates advance in place."""
@@ -459,6 +527,7 @@ def gaussian_stream(gstates, count: int, out=None, stream=None):
     return out
 
 
+@_on_device
 def to_text_dev(states, stream=None):
     """Bulk ranmar::to_text (serialize.hpp:21-40) on the GPU.
     Returns (text: uint8 CUDA tensor, offsets: int64 CUDA tensor [n + 1])."""
@@ -472,6 +541,7 @@ def to_text_dev(states, stream=None):
     return text, off
 
 
+@_on_device
 def from_text_dev(text, offsets, stream=None):
     """Bulk ranmar::from_text (serialize.hpp:81-136) on the GPU: texts
     [offsets[k], offsets[k+1]) of `text` -> (states [n, 100], err [n]); err[k]
@@ -500,6 +570,7 @@ def gauss_states_from(states_t):
     return g
 
 
+@_on_device
 def device_status(clear: bool = True) -> int:
     """Sticky status bits of the current device (bit 0: a state with bad cursors or v)."""
     flags = C.c_uint32()
@@ -516,8 +587,10 @@ class Context:
     """Host-buffer API (ranmar_ctx_*): the call a CPU-side user of the reference
     makes, with the host<->device copies inside."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: Optional[int] = None):
         self._h = C.c_void_p()
+        if device is None:  # the caller's current CUDA device
+            device = _torch().cuda.current_device()
         _check(lib().ranmar_ctx_create(device, C.byref(self._h)))
 
     def close(self):
@@ -594,7 +667,8 @@ class RanMars:
     _MIN_BLOCK = 256
 
     def __init__(self, seed: Optional[int] = None, state: Optional[np.ndarray] = None,
-                 block: int = 1 << 16, device: int = 0, ctx: Optional["Context"] = None):
+                 block: int = 1 << 16, device: Optional[int] = None,
+                 ctx: Optional["Context"] = None):
         if (seed is None) == (state is None):
             raise ValueError("give exactly one of seed or state")
         self._ctx = ctx or Context(device)

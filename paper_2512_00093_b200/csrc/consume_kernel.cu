@@ -157,12 +157,19 @@ __global__ void __launch_bounds__(kCT, 1)
 
 }  // namespace
 
+namespace {
+std::atomic<uint64_t> g_cfg_consume{0};
+}  // namespace
+
+cudaError_t configure_consume_kernel() {
+    return ensure_smem(consume_kernel, static_cast<int>(kConsumeSmem), g_cfg_consume);
+}
+
 cudaError_t launch_consume(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
                            uint64_t* d_sums, uint32_t* d_hist, uint32_t* status,
                            cudaStream_t stream) {
     if (n_streams == 0) return cudaSuccess;
-    static std::atomic<uint64_t> configured{0};
-    if (cudaError_t e = ensure_smem(consume_kernel, static_cast<int>(kConsumeSmem), configured)) return e;
+    if (cudaError_t e = ensure_smem(consume_kernel, static_cast<int>(kConsumeSmem), g_cfg_consume)) return e;
     const uint64_t blocks = (n_streams + kCT - 1) / kCT;
     count_launch();
     consume_kernel<<<static_cast<unsigned>(blocks), kCT, kConsumeSmem, stream>>>(

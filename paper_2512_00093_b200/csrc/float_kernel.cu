@@ -28,9 +28,14 @@ __device__ __forceinline__ int mod97f(int64_t x) {
 
 constexpr int kFWarps = 8;
 
+// kTrace: also store, per step, the value written into x[i] (y) and the new c
+// (the scalar step_float of the C++ facade copies them into the caller's
+// state, so every word of that state comes from this kernel).
+template <bool kTrace>
 __global__ void __launch_bounds__(32 * kFWarps)
     float_gen_kernel(ranmar_float_state* __restrict__ states, uint64_t n_streams, uint64_t N,
-                     double* __restrict__ out, uint32_t* status) {
+                     double* __restrict__ out, double* __restrict__ ty, double* __restrict__ tc,
+                     uint32_t* status) {
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kFWarps + (threadIdx.x >> 5);
     if (k >= n_streams) return;
     const int l = threadIdx.x & 31;
@@ -66,7 +71,13 @@ __global__ void __launch_bounds__(32 * kFWarps)
         R3 = R2;
         R2 = R1;
         R1 = y;
-        if (32 * r + l < N) o[32 * r] = fix1(y - c);
+        if (32 * r + l < N) {
+            o[32 * r] = fix1(y - c);
+            if (kTrace) {
+                ty[k * N + 32 * r + l] = y;
+                tc[k * N + 32 * r + l] = c;
+            }
+        }
         c += A32;
         if (c >= kModF) c -= kModF;
     }
@@ -92,12 +103,17 @@ __global__ void __launch_bounds__(32 * kFWarps)
 }  // namespace
 
 cudaError_t launch_float_gen(ranmar_float_state* d_states, uint64_t n_streams, uint64_t per_stream,
-                             double* d_out, uint32_t* status, cudaStream_t stream) {
+                             double* d_out, double* d_y, double* d_c, uint32_t* status,
+                             cudaStream_t stream) {
     if (n_streams == 0) return cudaSuccess;
     const uint64_t blocks = (n_streams + kFWarps - 1) / kFWarps;
     count_launch();
-    float_gen_kernel<<<static_cast<unsigned>(blocks), 32 * kFWarps, 0, stream>>>(
-        d_states, n_streams, per_stream, d_out, status);
+    if (d_y)
+        float_gen_kernel<true><<<static_cast<unsigned>(blocks), 32 * kFWarps, 0, stream>>>(
+            d_states, n_streams, per_stream, d_out, d_y, d_c, status);
+    else
+        float_gen_kernel<false><<<static_cast<unsigned>(blocks), 32 * kFWarps, 0, stream>>>(
+            d_states, n_streams, per_stream, d_out, nullptr, nullptr, status);
     return cudaGetLastError();
 }
 

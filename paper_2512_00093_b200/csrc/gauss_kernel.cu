@@ -4,7 +4,9 @@
 // defines it in oracle/ranmar_oracle.c (or_gaussian): Marsaglia polar method
 // on uniform() = next_f64 (core.hpp:70-72), v = 2u - 1, reject rsq >= 1 or
 // rsq == 0, return v2 * fac and cache v1 * fac (Numerical Recipes pairing),
-// log() being the fixed IEEE sequence or_glog so results are bit-identical.
+// log() being the correctly rounded crlog (gauss_math.cuh) so results are
+// bit-identical to the oracle and to RanMars::gaussian with a correctly
+// rounded libm log.
 //
 // Every gaussian() call consumes uniforms in pairs, so an atom's deviates are
 // the cached one (if has_saved) followed by (v2 fac, v1 fac) for each
@@ -192,8 +194,8 @@ __global__ void __launch_bounds__(kGT)
 
 // Self-check of div_rn / sqrt_rn against the library's __ddiv_rn / __dsqrt_rn
 // on the operands gaussian() can produce: rsq = s / 2^46 for pseudo-random
-// s in [1, 2^46) plus the range ends and powers of two; per value the glog
-// division f / (2 + f), the fac division and the sqrt are compared bitwise.
+// s in [1, 2^46) plus the range ends and powers of two; per value the fac
+// division and the sqrt are compared bitwise.
 __global__ void fp64_selfcheck_kernel(uint64_t n, uint64_t seed,
                                       unsigned long long* __restrict__ bad) {
     unsigned long long miss = 0;
@@ -204,16 +206,11 @@ __global__ void fp64_selfcheck_kernel(uint64_t n, uint64_t seed,
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
         uint64_t s = z & ((uint64_t(1) << 46) - 1);
-        if (k < 47) s = uint64_t(1) << k;  // powers of two: f = 0 in glog
+        if (k < 47) s = uint64_t(1) << k;  // powers of two: z = 0 in crlog
         if (k == 47) s = (uint64_t(1) << 46) - 1;
         if (s == 0 || s >= (uint64_t(1) << 46)) s = 1;
         const double rsq = static_cast<double>(s) * 0x1p-46;
-        const long long b = __double_as_longlong(rsq);
-        double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-        if (m > kGlogC[12]) m = __dmul_rn(m, 0.5);
-        const double f = __dsub_rn(m, 1.0), d = __dadd_rn(2.0, f);
-        miss += __double_as_longlong(div_rn(f, d)) != __double_as_longlong(__ddiv_rn(f, d));
-        const double num = __dmul_rn(-2.0, glog(rsq));
+        const double num = __dmul_rn(-2.0, crlog(rsq));
         const double q1 = div_rn(num, rsq), q2 = __ddiv_rn(num, rsq);
         miss += __double_as_longlong(q1) != __double_as_longlong(q2);
         miss += __double_as_longlong(sqrt_rn(q2)) != __double_as_longlong(__dsqrt_rn(q2));
@@ -229,13 +226,57 @@ cudaError_t launch_fp64_selfcheck(uint64_t n, uint64_t seed, unsigned long long*
     return cudaGetLastError();
 }
 
+// Exhaustive check of crlog on gaussian()'s domain: rsq = s / 2^46 for
+// s in [s0, s0 + n). counts[0] = inputs whose fast phase did not decide,
+// counts[1] = inputs whose accurate phase did not decide either (the claim
+// "correctly rounded on the whole domain" needs 0 over all 2^46 - 1 inputs),
+// counts[2] = (mode 1 only) inputs where the fast phase decided a value other
+// than the accurate phase's, counts[3] = number of inputs recorded; their s
+// values go to fails[0 .. cap) for the CPU to re-check against the oracle and
+// mpmath: the fast-phase failures (modes 0, 1) or only the accurate-phase
+// failures (mode 2).
+__global__ void crlog_sweep_kernel(uint64_t s0, uint64_t n, int mode,
+                                   unsigned long long* __restrict__ counts,
+                                   uint64_t* __restrict__ fails, uint64_t cap) {
+    unsigned long long nfast = 0, nacc = 0, nmis = 0;
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t s = s0 + k;
+        const double x = static_cast<double>(s) * 0x1p-46;
+        bool fast;
+        const double y = crlog(x, &fast);
+        if (!fast) {
+            ++nfast;
+            const bool undecided = crlog_accurate(x).ok == 0;
+            nacc += undecided;
+            if (mode != 2 || undecided) {  // mode 2 records only accurate-phase failures
+                const unsigned long long slot = atomicAdd(counts + 3, 1ull);
+                if (slot < cap) fails[slot] = s;
+            }
+        } else if (mode == 1) {
+            const CrlogAcc a = crlog_accurate(x);
+            nacc += a.ok == 0;
+            nmis += __double_as_longlong(a.y) != __double_as_longlong(y);
+        }
+    }
+    if (nfast) atomicAdd(counts + 0, nfast);
+    if (nacc) atomicAdd(counts + 1, nacc);
+    if (nmis) atomicAdd(counts + 2, nmis);
+}
+
+cudaError_t launch_crlog_sweep(uint64_t s0, uint64_t n, int mode, unsigned long long* d_counts,
+                               uint64_t* d_fails, uint64_t cap, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    crlog_sweep_kernel<<<148 * 8, 256, 0, stream>>>(s0, n, mode, d_counts, d_fails, cap);
+    return cudaGetLastError();
+}
+
 template <int K>
 cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                               uint64_t steps, double* d_out, uint32_t* status,
                               cudaStream_t stream) {
-    const int smem = 97 * kGT * 4;
-    static std::atomic<uint64_t> configured{0};
-    if (cudaError_t e = ensure_smem(gaussian_kernel<K>, smem, configured)) return e;
+    const int smem = 97 * kGT * 4;  // 24.8 KB: within the default 48 KB limit
     const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
     count_launch();
     gaussian_kernel<K><<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(

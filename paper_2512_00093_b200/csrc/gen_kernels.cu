@@ -64,7 +64,9 @@ struct WarpGen {
         return true;
     }
 
-    // One round: returns x_n - v_n (unmasked) for n = 32 r + l.
+    // One round: returns x_n - v_n (unmasked) for n = 32 r + l; x_n (unmasked)
+    // and v_n are left in R1 and last_v.
+    uint32_t last_v;
     __device__ __forceinline__ uint32_t round() {
         const uint32_t S = __shfl_sync(0xffffffffu, R3 - R1, src);
         const uint32_t y = (l == 0) ? prev : S;
@@ -74,6 +76,7 @@ struct WarpGen {
         R2 = R1;
         R1 = y;
         const uint32_t raw = y - V;
+        last_v = V;
         V = add_mod_m(V, A32);
         return raw;
     }
@@ -150,14 +153,48 @@ __global__ void __launch_bounds__(32 * kGenWarps)
     });
 }
 
+// Trace of N steps per stream (the scalar step() of the C++ facade): u[n] =
+// output n, x[n] = the value step n writes into lane[i] (x_n), v[n] = the
+// residue after step n. States advance like gen_store_kernel.
+__global__ void __launch_bounds__(32 * kGenWarps)
+    gen_trace_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
+                     uint32_t* __restrict__ uo, uint32_t* __restrict__ xo, uint32_t* __restrict__ vo,
+                     uint32_t* status) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kGenWarps + (threadIdx.x >> 5);
+    if (k >= n_streams) return;
+    const uint64_t base = k * per_stream + (threadIdx.x & 31);
+    WarpGen g;
+    if (!g.load(states + k, status)) return;
+    const uint64_t rounds = (per_stream + 31) >> 5;
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint32_t raw = g.round();
+        if (32 * r + g.l < per_stream) {
+            uo[base + 32 * r] = raw & kMask;
+            xo[base + 32 * r] = g.R1 & kMask;
+            vo[base + 32 * r] = g.last_v;
+        }
+    }
+    g.store(states + k, per_stream, rounds);
+}
+
 // One stream generated as P substreams (ranmar_generate_single_*): the final
 // state is the last substream's, re-laid in the ORIGINAL ring layout, i.e.
 // exactly what `count` calls of step() leave: canonical u[k] = lane[(i - k)
 // mod 97] is layout-independent, and lane[(i_t - k) mod 97] = u[k] with the
-// target cursor i_t = (i0 - count) mod 97 (jump.hpp:32-48).
+// target cursor i_t = (i0 - count) mod 97 (jump.hpp:32-48). i0 is read from
+// dst (the original state) before it is overwritten; an invalid original state
+// was already flagged by make_streams and is left untouched.
 __global__ void relayout_kernel(const ranmar_state* __restrict__ src, ranmar_state* __restrict__ dst,
-                                int i_t) {
+                                int count_mod97) {
+    __shared__ int s_it;
     const int k = threadIdx.x;
+    if (k == 0) {
+        const int i0 = dst->i;
+        s_it = state_ok(i0, dst->j, dst->v) ? (i0 - count_mod97 + 97) % 97 : -1;
+    }
+    __syncthreads();
+    const int i_t = s_it;
+    if (i_t < 0) return;
     if (k < 97) {
         int q = src->i - k;
         q += q < 0 ? 97 : 0;
@@ -176,10 +213,21 @@ __global__ void relayout_kernel(const ranmar_state* __restrict__ src, ranmar_sta
 
 // ---------------------------------------------------------------- launchers
 
-cudaError_t launch_relayout(const ranmar_state* src, ranmar_state* dst, int i_t,
+cudaError_t launch_relayout(const ranmar_state* src, ranmar_state* dst, int count_mod97,
                             cudaStream_t stream) {
     count_launch();
-    relayout_kernel<<<1, 128, 0, stream>>>(src, dst, i_t);
+    relayout_kernel<<<1, 128, 0, stream>>>(src, dst, count_mod97);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate_trace(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                                  uint32_t* d_u, uint32_t* d_x, uint32_t* d_v, uint32_t* status,
+                                  cudaStream_t stream) {
+    if (n_streams == 0 || per_stream == 0) return cudaSuccess;
+    const uint64_t blocks = (n_streams + kGenWarps - 1) / kGenWarps;
+    count_launch();
+    gen_trace_kernel<<<static_cast<unsigned>(blocks), 32 * kGenWarps, 0, stream>>>(
+        d_states, n_streams, per_stream, d_u, d_x, d_v, status);
     return cudaGetLastError();
 }
 

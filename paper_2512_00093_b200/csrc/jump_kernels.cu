@@ -134,6 +134,32 @@ __device__ __forceinline__ void block_mul_t(uint32_t* a) {
 
 __device__ __forceinline__ bool ebit(const uint64_t* e, int b) { return (e[b >> 6] >> (b & 63)) & 1u; }
 
+// Polynomial primitives for the C++ facade's ranmar::poly (polyring.hpp:60-98),
+// one 256-thread CTA per item: mode 0 out = a * b mod phi (mul_mod, items of 97
+// words), mode 1 out = raw mod phi (reduce_trinomial, a = items of 193 raw
+// words, wrapping u32 fold like the reference's).
+__global__ void __launch_bounds__(kPowThreads)
+    poly_kernel(int mode, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                uint32_t* __restrict__ out) {
+    __shared__ uint32_t sa[kPolyN], sb[kPolyN], so[kPolyN];
+    __shared__ BlockMulScratch scr;
+    const uint64_t q = blockIdx.x;
+    const int t = threadIdx.x;
+    if (mode == 0) {
+        if (t < kPolyN) {
+            sa[t] = a[q * kPolyN + t];
+            sb[t] = b[q * kPolyN + t];
+        }
+        __syncthreads();
+        block_mulmod(sa, sb, so, scr);
+    } else {
+        if (t < 193) scr.c[t] = a[q * 193 + t];
+        __syncthreads();
+        fold_to(scr.c, so, t, kPowThreads, [] { __syncthreads(); });
+    }
+    if (t < kPolyN) out[q * kPolyN + t] = so[t];
+}
+
 __global__ void __launch_bounds__(kPowThreads) pow_kernel(PowJobs jobs) {
     __shared__ uint32_t a[kPolyN];
     __shared__ BlockMulScratch c;
@@ -503,6 +529,32 @@ __global__ void put_state_kernel(ranmar_state s, ranmar_state* dst) {
     for (int k = threadIdx.x; k < 100; k += blockDim.x) d[k] = src[k];
 }
 
+// A device-resident base state copied into the workspace and checked there
+// (the host path checks it before launching): cursors, v and every lane must
+// satisfy the reference's invariants. A bad state raises kStatusBadState and is
+// replaced by the all-zero state with fresh cursors, so no later kernel indexes
+// out of range.
+__global__ void copy_state_kernel(const ranmar_state* __restrict__ src, ranmar_state* __restrict__ dst,
+                                  uint32_t* status) {
+    __shared__ int bad;
+    const int k = threadIdx.x;
+    if (k == 0) bad = !state_ok(src->i, src->j, src->v);
+    __syncthreads();
+    if (k < 97 && src->lane[k] > kMask) bad = 1;
+    __syncthreads();
+    if (bad) {
+        if (k == 0) atomicOr(status, kStatusBadState);
+        if (k < 97) dst->lane[k] = 0;
+        if (k == 0) {
+            dst->i = 96;
+            dst->j = 32;
+            dst->v = 0;
+        }
+        return;
+    }
+    if (k < 100) reinterpret_cast<uint32_t*>(dst)[k] = reinterpret_cast<const uint32_t*>(src)[k];
+}
+
 // ---- make_streams bulk (level 0): s_{(first + 128 h + r) J} = apply(anchor_h, T_r).
 // Per anchor a 128 x 97 x 97 integer "GEMM" tile on the IMAD pipe:
 //  * T^T (97 x 128) stays in shared memory for every anchor the CTA visits;
@@ -527,15 +579,15 @@ struct BulkArgs {
     const uint32_t* Tt;   // [97][128]
     ranmar_state* out;    // streams [first, first + n)
     uint64_t first, n;
-    uint32_t v_base;      // v of the base state
-    uint32_t jm;          // J mod m
-    ranmar_state base;    // stream 0 verbatim (when first == 0)
+    uint32_t jm;                // J mod m
+    const ranmar_state* base;   // the base state in device memory (stream 0 when first == 0)
 };
 
 // Record tail of row `row` of anchor h: word 96 (column 0, summed in C0), the
 // normalised cursors and v (closed form, jump_arith with k J mod m); zeroes the
 // row's accumulator for the anchor after next.
-__device__ __forceinline__ void bulk_tail(const BulkArgs& args, uint32_t* C0, uint64_t h, int row) {
+__device__ __forceinline__ void bulk_tail(const BulkArgs& args, uint32_t v_base, uint32_t* C0,
+                                          uint64_t h, int row) {
     const uint32_t a0 = C0[row];
     C0[row] = 0;
     const uint64_t row0 = h * kRows;
@@ -543,7 +595,7 @@ __device__ __forceinline__ void bulk_tail(const BulkArgs& args, uint32_t* C0, ui
     if (static_cast<uint64_t>(row) >= rows || (args.first == 0 && h == 0 && row == 0)) return;
     const uint64_t k = args.first + row0 + row;
     const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
-    const uint32_t v = static_cast<uint32_t>((args.v_base + (kMod - dec)) % kMod);
+    const uint32_t v = static_cast<uint32_t>((v_base + (kMod - dec)) % kMod);
     *reinterpret_cast<uint4*>(args.out[row0 + row].lane + 96) = make_uint4(a0 & kMask, 96u, 32u, v);
 }
 
@@ -587,6 +639,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
     const int g = t >> 5, rg = t & 31;
     const int m0 = 89 - 8 * g;
     const uint64_t G = gridDim.x;
+    const uint32_t v_base = args.base->v;
 
     {   // T^T tile, loaded once per CTA
         const uint4* src = reinterpret_cast<const uint4*>(args.Tt);
@@ -611,7 +664,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
         const uint32_t* W = Wb + slot * kWAnchor;
         if (it >= 2) {
             wait_end(it - 2);  // W[slot] (prefetched in it - 2) and C0 of anchor it - 2 are complete
-            if (t < kRows) bulk_tail(args, C0 + ((it - 2) % 3) * kRows, h - 2 * G, t);
+            if (t < kRows) bulk_tail(args, v_base, C0 + ((it - 2) % 3) * kRows, h - 2 * G, t);
         }
         uint32_t acc[4][8];
         uint32_t win[8];
@@ -658,7 +711,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
                                 acc[rr][0] & kMask);
         }
         if (skip0 && t < 100)
-            reinterpret_cast<uint32_t*>(args.out)[t] = reinterpret_cast<const uint32_t*>(&args.base)[t];
+            reinterpret_cast<uint32_t*>(args.out)[t] = reinterpret_cast<const uint32_t*>(args.base)[t];
         // W[(it + 2) % 3] and C0[slot]: their last readers / the tail that zeroed
         // C0[slot] ran in iteration it - 1
         if (it >= 1) wait_end(it - 1);
@@ -678,13 +731,21 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
     // tails of the last two anchors
     for (int k = it >= 2 ? it - 2 : 0; k < it; ++k) {
         wait_end(k);
-        if (t < kRows) bulk_tail(args, C0 + (k % 3) * kRows, h0 + static_cast<uint64_t>(k) * G, t);
+        if (t < kRows) bulk_tail(args, v_base, C0 + (k % 3) * kRows, h0 + static_cast<uint64_t>(k) * G, t);
     }
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+
+cudaError_t launch_poly(int mode, const uint32_t* a, const uint32_t* b, uint32_t* out, uint64_t n,
+                        cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    poly_kernel<<<static_cast<unsigned>(n), kPowThreads, 0, stream>>>(mode, a, b, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pow(const PowJobs& jobs, int njobs, cudaStream_t stream) {
     count_launch();
@@ -716,11 +777,21 @@ cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t
     return cudaGetLastError();
 }
 
+namespace {
+std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0};
+}  // namespace
+
+// Shared-memory limits of the jump kernels, raised by ranmar_device_setup so no
+// _dev call (or graph capture) has to do it.
+cudaError_t configure_jump_kernels() {
+    if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
+    return ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk);
+}
+
 cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, const uint32_t* P,
                          uint32_t dec, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
-    static std::atomic<uint64_t> configured{0};
-    if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), configured)) return e;
+    if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
     count_launch();
     apply2_kernel<<<static_cast<unsigned>((n + kA2Items - 1) / kA2Items), kA2Threads, kA2Smem,
                     stream>>>(in, out, n, P, dec);
@@ -747,12 +818,18 @@ cudaError_t launch_put_state(const ranmar_state& s, ranmar_state* dst, cudaStrea
     return cudaGetLastError();
 }
 
+cudaError_t launch_copy_state(const ranmar_state* src, ranmar_state* dst, uint32_t* status,
+                              cudaStream_t stream) {
+    count_launch();
+    copy_state_kernel<<<1, 128, 0, stream>>>(src, dst, status);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
-                        uint64_t first, uint64_t n, uint32_t v_base, uint32_t jm,
-                        const ranmar_state& base, int sm_count, cudaStream_t stream) {
-    static std::atomic<uint64_t> configured{0};
-    if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), configured)) return e;
-    BulkArgs a{W1, H, Tt, out, first, n, v_base, jm, base};
+                        uint64_t first, uint64_t n, uint32_t jm, const ranmar_state* d_base,
+                        int sm_count, cudaStream_t stream) {
+    if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk)) return e;
+    BulkArgs a{W1, H, Tt, out, first, n, jm, d_base};
     const uint64_t grid = H < uint64_t(2 * sm_count) ? H : uint64_t(2 * sm_count);
     count_launch();
     bulk_kernel<<<static_cast<unsigned>(grid), kBulkThreads, kBulkSmem, stream>>>(a);

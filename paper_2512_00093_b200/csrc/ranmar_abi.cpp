@@ -14,6 +14,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
+#include <initializer_list>
 
 #include "ranmar_b200.h"
 
@@ -32,8 +34,11 @@ cudaError_t launch_consume(ranmar_state*, uint64_t, uint64_t, uint64_t*, uint32_
                            cudaStream_t);
 cudaError_t launch_gaussian_stream(ranmar_gauss_state*, uint64_t, uint64_t, double*, uint32_t*,
                                    cudaStream_t);
-cudaError_t launch_float_gen(ranmar_float_state*, uint64_t, uint64_t, double*, uint32_t*,
-                             cudaStream_t);
+cudaError_t launch_float_gen(ranmar_float_state*, uint64_t, uint64_t, double*, double*, double*,
+                             uint32_t*, cudaStream_t);
+cudaError_t launch_generate_trace(ranmar_state*, uint64_t, uint64_t, uint32_t*, uint32_t*, uint32_t*,
+                                  uint32_t*, cudaStream_t);
+cudaError_t launch_poly(int, const uint32_t*, const uint32_t*, uint32_t*, uint64_t, cudaStream_t);
 uint64_t text_bound(uint64_t);
 size_t text_workspace(uint64_t);
 cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void*, cudaStream_t);
@@ -52,6 +57,8 @@ cudaError_t launch_langevin_bank(uint32_t*, uint64_t, uint64_t, const double*, d
                                  uint32_t*, cudaStream_t);
 cudaError_t launch_relayout(const ranmar_state*, ranmar_state*, int, cudaStream_t);
 cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
+cudaError_t launch_crlog_sweep(uint64_t, uint64_t, int, unsigned long long*, uint64_t*, uint64_t,
+                               cudaStream_t);
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
                              const uint32_t*, cudaStream_t);
@@ -61,8 +68,11 @@ cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uin
 cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
                          uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
+cudaError_t launch_copy_state(const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
 cudaError_t launch_bulk(const uint32_t*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
-                        uint64_t, uint32_t, uint32_t, const ranmar_state&, int, cudaStream_t);
+                        uint64_t, uint32_t, const ranmar_state*, int, cudaStream_t);
+cudaError_t configure_jump_kernels();
+cudaError_t configure_consume_kernel();
 std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 }  // namespace rb
@@ -135,53 +145,71 @@ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
 // (J mod m) * d mod m: the per-jump decrement of the arithmetic part (jump.hpp:82-84).
 uint32_t arith_dec(uint32_t jm) { return static_cast<uint32_t>(mulmod(jm, kDelta, kMod)); }
 
-// ---- per-device status word and SM count ---------------------------------
+// ---- per-device resources -------------------------------------------------
+// Built once per device by ranmar_device_setup (the only entry point besides
+// the ctx_* pipeline that allocates or synchronises): the sticky status word,
+// the SM count, and the table of squares Z_k = t^(2^k) mod phi (k < kSquares),
+// the squaring half of square-and-multiply, independent of any J, built by
+// pow_kernel's squaring chain. The _dev entry points only read them, so they
+// never allocate or synchronise and can be captured in a CUDA graph.
+struct DevRes {
+    uint32_t* status = nullptr;
+    uint32_t* squares = nullptr;
+    int sms = 0;
+};
 std::mutex g_dev_mu;
-uint32_t* g_status[64] = {};
-int g_sms[64] = {};
+DevRes g_res[64];
+std::atomic<bool> g_ready[64];
+
+int current_res(const DevRes** out) {
+    int dev = 0;
+    RB_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(RANMAR_ECUDA, "ranmar: device index out of range");
+    if (!g_ready[dev].load(std::memory_order_acquire))
+        return fail(RANMAR_ESTATE, "ranmar: device " + std::to_string(dev) +
+                                       " is not set up: call ranmar_device_setup(" +
+                                       std::to_string(dev) + ", stream) once first");
+    *out = &g_res[dev];
+    return RANMAR_OK;
+}
+
+// ctx_* calls route the kernels' status bits to their context's own word
+thread_local uint32_t* g_status_override = nullptr;
 
 int device_status_ptr(uint32_t** out, int* sms) {
-    int dev = 0;
-    RB_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-    if (dev < 0 || dev >= 64) return fail(RANMAR_ECUDA, "ranmar: device index out of range");
-    std::lock_guard<std::mutex> lk(g_dev_mu);
-    if (!g_status[dev]) {
-        uint32_t* p = nullptr;
-        RB_CUDA(cudaMalloc(&p, 256), "cudaMalloc(status)");
-        RB_CUDA(cudaMemset(p, 0, 256), "cudaMemset(status)");
-        RB_CUDA(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev),
-                "cudaDeviceGetAttribute");
-        g_status[dev] = p;
-    }
-    *out = g_status[dev];
-    if (sms) *sms = g_sms[dev];
+    const DevRes* r = nullptr;
+    if (int rc = current_res(&r)) return rc;
+    *out = g_status_override ? g_status_override : r->status;
+    if (sms) *sms = r->sms;
     return RANMAR_OK;
 }
 
-// ---- per-device square table Z_k = t^(2^k) mod phi (k < kSquares) --------
-// The squaring half of square-and-multiply, independent of any J: built once
-// per device by pow_kernel's squaring chain and kept for the process.
-uint32_t* g_squares[64] = {};
-
-int square_table(const uint32_t** out, cudaStream_t s) {
-    int dev = 0;
-    RB_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-    if (dev < 0 || dev >= 64) return fail(RANMAR_ECUDA, "ranmar: device index out of range");
-    std::lock_guard<std::mutex> lk(g_dev_mu);
-    if (!g_squares[dev]) {
-        uint32_t* z = nullptr;
-        RB_CUDA(cudaMalloc(&z, size_t(kSquares) * kPolyN * 4), "cudaMalloc(squares)");
-        rb::PowJobs jobs{};
-        jobs.job[0].e[0] = 1;  // t^1, then kSquares - 1 squarings
-        jobs.job[0].extra = kSquares - 1;
-        jobs.job[0].out = z;
-        RB_CUDA(rb::launch_pow(jobs, 1, s), "pow_kernel launch (square table)");
-        RB_CUDA(cudaStreamSynchronize(s), "square table build");
-        g_squares[dev] = z;
-    }
-    *out = g_squares[dev];
+int square_table(const uint32_t** out) {
+    const DevRes* r = nullptr;
+    if (int rc = current_res(&r)) return rc;
+    *out = r->squares;
     return RANMAR_OK;
 }
+
+// Makes `device` current for a scope and restores the caller's device after.
+class DeviceGuard {
+  public:
+    cudaError_t enter(int device) {
+        cudaError_t e = cudaGetDevice(&prev_);
+        if (e != cudaSuccess) {
+            prev_ = -1;
+            return e;
+        }
+        return prev_ == device ? cudaSuccess : cudaSetDevice(device);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev_ >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev_) cudaSetDevice(prev_);
+    }
+
+  private:
+    int prev_ = -1;
+};
 
 // ---- make_streams workspace plan -----------------------------------------
 // Stream starts form a base-128 tree: level L holds count[L] = ceil(n / 128^L)
@@ -256,9 +284,14 @@ void seed_expand(uint32_t seed, ranmar_state* out) {
     out->v = kStart;
 }
 
+// The reference's invariants of RanmarState (core.hpp:29-49): 24-bit lanes,
+// 0-based cursors with (i - j) mod 97 = 64, v < m.
 bool host_state_ok(const ranmar_state& s) {
-    return s.i >= 0 && s.i < 97 && s.j >= 0 && s.j < 97 && (s.i - s.j + 97) % 97 == 64 &&
-           s.v < kMod;
+    if (!(s.i >= 0 && s.i < 97 && s.j >= 0 && s.j < 97 && (s.i - s.j + 97) % 97 == 64 && s.v < kMod))
+        return false;
+    for (int k = 0; k < 97; ++k)
+        if (s.lane[k] > kMask) return false;
+    return true;
 }
 
 }  // namespace
@@ -267,6 +300,36 @@ bool host_state_ok(const ranmar_state& s) {
 extern "C" {
 
 int ranmar_abi_version(void) { return RANMAR_ABI_VERSION; }
+
+int ranmar_device_setup(int device, void* stream) {
+    int count = 0;
+    RB_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count || device >= 64)
+        return fail(RANMAR_ECUDA, "ranmar: no such CUDA device");
+    if (g_ready[device].load(std::memory_order_acquire)) return RANMAR_OK;
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_ready[device].load(std::memory_order_relaxed)) return RANMAR_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevRes r;
+    RB_CUDA(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, device),
+            "cudaDeviceGetAttribute");
+    RB_CUDA(cudaMalloc(&r.status, 256), "cudaMalloc(status)");
+    RB_CUDA(cudaMemsetAsync(r.status, 0, 256, s), "cudaMemset(status)");
+    RB_CUDA(cudaMalloc(&r.squares, size_t(kSquares) * kPolyN * 4), "cudaMalloc(squares)");
+    rb::PowJobs jobs{};
+    jobs.job[0].e[0] = 1;  // t^1, then kSquares - 1 squarings
+    jobs.job[0].extra = kSquares - 1;
+    jobs.job[0].out = r.squares;
+    RB_CUDA(rb::launch_pow(jobs, 1, s), "pow_kernel launch (square table)");
+    RB_CUDA(cudaStreamSynchronize(s), "square table build");
+    RB_CUDA(rb::configure_jump_kernels(), "cudaFuncSetAttribute (jump kernels)");
+    RB_CUDA(rb::configure_consume_kernel(), "cudaFuncSetAttribute (consume kernel)");
+    g_res[device] = r;
+    g_ready[device].store(true, std::memory_order_release);
+    return RANMAR_OK;
+}
 uint64_t ranmar_kernel_launches(void) { return rb::g_launches.load(); }
 const char* ranmar_last_error(void) { return g_error.c_str(); }
 
@@ -449,7 +512,7 @@ int ranmar_pow_t_mod_dev(const ranmar_jump_count* j, uint32_t* d_coeff, void* st
     if (!j || !d_coeff) return fail(RANMAR_EINVAL, "ranmar: null argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t* Z = nullptr;
-    if (int rc = square_table(&Z, s)) return rc;
+    if (int rc = square_table(&Z)) return rc;
     const uint64_t(*e)[4] = &j->limb;
     const int shift = 0;
     uint32_t* out = d_coeff;
@@ -472,14 +535,21 @@ int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
     return RANMAR_OK;
 }
 
-int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j, uint64_t first,
-                            uint64_t n, ranmar_state* d_out, void* d_ws, size_t ws_bytes,
-                            void* stream) {
-    if (!base || !j) return fail(RANMAR_EINVAL, "ranmar: null argument");
+}  // extern "C"
+
+namespace {
+
+// make_streams for a base state given on the host (h_base, checked here) or in
+// device memory (d_base, checked by copy_state_kernel, which flags the status
+// word): exactly one of them is non-null.
+int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
+                      const ranmar_jump_count* j, uint64_t first, uint64_t n, ranmar_state* d_out,
+                      void* d_ws, size_t ws_bytes, void* stream) {
+    if (!j) return fail(RANMAR_EINVAL, "ranmar: null argument");
     if (n == 0) return fail(RANMAR_EINVAL, "ranmar: need at least one stream");  // jump.hpp:111
     const U256 J = from_abi(j);
     if (is_zero(J)) return fail(RANMAR_EINVAL, "ranmar: block length must be >= 1");  // :112
-    if (!host_state_ok(*base))
+    if (h_base && !host_state_ok(*h_base))
         return fail(RANMAR_ESTATE, "ranmar: base state violates cursor/residue invariants");
     if (first >= (uint64_t(1) << 62) || n >= (uint64_t(1) << 62) || first + n >= (uint64_t(1) << 62))
         return fail(RANMAR_ERANGE, "ranmar: stream range too large");
@@ -496,10 +566,9 @@ int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j
     int sms = 148;
     uint32_t* status = nullptr;
     if (int rc = device_status_ptr(&status, &sms)) return rc;
-    (void)status;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t* Z = nullptr;
-    if (int rc = square_table(&Z, s)) return rc;
+    if (int rc = square_table(&Z)) return rc;
     char* ws = static_cast<char*>(d_ws);
     uint32_t* Q = reinterpret_cast<uint32_t*>(ws + p.off_q);
     uint32_t* Pf = reinterpret_cast<uint32_t*>(ws + p.off_pfirst);
@@ -530,18 +599,22 @@ int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j
     RB_CUDA(rb::launch_pow_table(e, shift, outs, njobs, Z, s), "pow_table_kernel launch");
     // Offset tables Tab_L[r] = P_{r 128^L J}.
     RB_CUDA(rb::launch_tables(Q, p.tab_levels, Tab, Tt, s), "tables_kernel launch");
-    // A_0 = s_{first J}.
-    const uint32_t jm = mod_u32(J, kMod);
-    if (first == 0) {
-        RB_CUDA(rb::launch_put_state(*base, A0, s), "put_state launch");
+    // The base state, in the workspace; A_0 = s_{first J}.
+    if (h_base) {
+        RB_CUDA(rb::launch_put_state(*h_base, dbase, s), "put_state launch");
     } else {
-        RB_CUDA(rb::launch_put_state(*base, dbase, s), "put_state launch");
+        RB_CUDA(rb::launch_copy_state(d_base, dbase, status, s), "copy_state launch");
+    }
+    const uint32_t jm = mod_u32(J, kMod);
+    const ranmar_state* a0 = dbase;
+    if (first > 0) {
         const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(first % kMod, jm, kMod)));
         RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, s), "apply_kernel launch");
+        a0 = A0;
     }
     // Levels L-1 .. 1 of the base-128 tree (level 1 writes the anchors'
     // extensions for the bulk kernel), then level 0.
-    const ranmar_state* in = A0;
+    const ranmar_state* in = a0;
     for (int L = p.top - 1; L >= 1; --L) {
         uint64_t pw = 1;  // 128^L mod m
         for (int x = 0; x < L; ++x) pw = pw * 128 % kMod;
@@ -556,9 +629,27 @@ int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j
             in = o;
         }
     }
-    RB_CUDA(rb::launch_bulk(W1, p.count[1], Tt, d_out, first, n, base->v, jm, *base, sms, s),
+    RB_CUDA(rb::launch_bulk(W1, p.count[1], Tt, d_out, first, n, jm, dbase, sms, s),
             "bulk_kernel launch");
     return RANMAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ranmar_make_streams_dev(const ranmar_state* base, const ranmar_jump_count* j, uint64_t first,
+                            uint64_t n, ranmar_state* d_out, void* d_ws, size_t ws_bytes,
+                            void* stream) {
+    if (!base) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    return make_streams_impl(base, nullptr, j, first, n, d_out, d_ws, ws_bytes, stream);
+}
+
+int ranmar_make_streams_from_dev(const ranmar_state* d_base, const ranmar_jump_count* j,
+                                 uint64_t first, uint64_t n, ranmar_state* d_out, void* d_ws,
+                                 size_t ws_bytes, void* stream) {
+    if (!d_base) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    return make_streams_impl(nullptr, d_base, j, first, n, d_out, d_ws, ws_bytes, stream);
 }
 
 #define RB_STATUS_PTR(var)                               \
@@ -612,23 +703,18 @@ int generate_single(ranmar_state* d_state, uint64_t count, T* d_out, void* d_ws,
     if (!d_ws) return fail(RANMAR_EINVAL, "ranmar: null workspace");
     if (ws_bytes < need) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    ranmar_state base;
-    RB_CUDA(cudaMemcpyAsync(&base, d_state, sizeof base, cudaMemcpyDeviceToHost, s), "D2H state");
-    RB_CUDA(cudaStreamSynchronize(s), "sync");
-    if (!host_state_ok(base))
-        return fail(RANMAR_ESTATE, "ranmar: state violates cursor/residue invariants");
+    // substream k = s_{k L} from the device-resident state itself (no host read)
     ranmar_state* sub = static_cast<ranmar_state*>(d_ws);
     char* ws2 = static_cast<char*>(d_ws) + single_ws_states(parts);
     ranmar_jump_count J = {{kSingleL, 0, 0, 0}};
-    if (int rc = ranmar_make_streams_dev(&base, &J, 0, parts, sub, ws2, ws_bytes - single_ws_states(parts),
-                                         stream))
+    if (int rc = make_streams_impl(nullptr, d_state, &J, 0, parts, sub, ws2,
+                                   ws_bytes - single_ws_states(parts), stream))
         return rc;
     if (int rc = gen(sub, parts - 1, kSingleL, d_out, stream)) return rc;
     const uint64_t last = count - (parts - 1) * kSingleL;
     if (int rc = gen(sub + parts - 1, 1, last, d_out + (parts - 1) * kSingleL, stream)) return rc;
-    int i_t = static_cast<int>((static_cast<int64_t>(base.i) - static_cast<int64_t>(count % 97)) % 97);
-    i_t += i_t < 0 ? 97 : 0;
-    RB_CUDA(rb::launch_relayout(sub + parts - 1, d_state, i_t, s), "relayout_kernel launch");
+    RB_CUDA(rb::launch_relayout(sub + parts - 1, d_state, static_cast<int>(count % 97), s),
+            "relayout_kernel launch");
     return RANMAR_OK;
 }
 
@@ -748,6 +834,17 @@ int ranmar_fp64_selfcheck_dev(uint64_t n, uint64_t seed, unsigned long long* d_m
     return RANMAR_OK;
 }
 
+int ranmar_crlog_sweep_dev(uint64_t s0, uint64_t n, int32_t mode, unsigned long long* d_counts,
+                           uint64_t* d_fails, uint64_t cap, void* stream) {
+    if (n && (!d_counts || (cap && !d_fails))) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (mode < 0 || mode > 2) return fail(RANMAR_EINVAL, "ranmar: crlog sweep mode must be 0, 1 or 2");
+    if (s0 == 0 || s0 + n > (uint64_t(1) << 46) || s0 + n < s0)
+        return fail(RANMAR_EINVAL, "ranmar: crlog sweep range must lie in [1, 2^46)");
+    RB_CUDA(rb::launch_crlog_sweep(s0, n, mode, d_counts, d_fails, cap, static_cast<cudaStream_t>(stream)),
+            "crlog_sweep_kernel launch");
+    return RANMAR_OK;
+}
+
 int ranmar_init_float(uint32_t seed, ranmar_float_state* out) {
     ranmar_state s;
     if (int rc = ranmar_init(seed, &s)) return rc;
@@ -763,9 +860,52 @@ int ranmar_generate_float_dev(ranmar_float_state* d_states, uint64_t n_streams,
     if (n_streams && (!d_states || (per_stream && !d_out)))
         return fail(RANMAR_EINVAL, "ranmar: null device buffer");
     RB_STATUS_PTR(status);
-    RB_CUDA(rb::launch_float_gen(d_states, n_streams, per_stream, d_out, status,
+    RB_CUDA(rb::launch_float_gen(d_states, n_streams, per_stream, d_out, nullptr, nullptr, status,
                                  static_cast<cudaStream_t>(stream)),
             "float_gen_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_generate_float_trace_dev(ranmar_float_state* d_states, uint64_t n_streams,
+                                    uint64_t per_stream, double* d_out, double* d_y, double* d_c,
+                                    void* stream) {
+    if (n_streams && per_stream && (!d_states || !d_out || !d_y || !d_c))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (per_stream == 0) return RANMAR_OK;
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_float_gen(d_states, n_streams, per_stream, d_out, d_y, d_c, status,
+                                 static_cast<cudaStream_t>(stream)),
+            "float_gen_kernel<trace> launch");
+    return RANMAR_OK;
+}
+
+int ranmar_generate_trace_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                              uint32_t* d_u, uint32_t* d_x, uint32_t* d_v, void* stream) {
+    if (n_streams && per_stream && (!d_states || !d_u || !d_x || !d_v))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_generate_trace(d_states, n_streams, per_stream, d_u, d_x, d_v, status,
+                                      static_cast<cudaStream_t>(stream)),
+            "gen_trace_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_poly_mul_mod_dev(const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n,
+                            void* stream) {
+    if (n && (!d_a || !d_b || !d_out)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    const DevRes* r = nullptr;
+    if (int rc = current_res(&r)) return rc;
+    RB_CUDA(rb::launch_poly(0, d_a, d_b, d_out, n, static_cast<cudaStream_t>(stream)),
+            "poly_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_poly_reduce_dev(const uint32_t* d_raw, uint32_t* d_out, uint64_t n, void* stream) {
+    if (n && (!d_raw || !d_out)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    const DevRes* r = nullptr;
+    if (int rc = current_res(&r)) return rc;
+    RB_CUDA(rb::launch_poly(1, d_raw, nullptr, d_out, n, static_cast<cudaStream_t>(stream)),
+            "poly_kernel launch");
     return RANMAR_OK;
 }
 
@@ -803,8 +943,16 @@ int ranmar_gaussian_stream_f64_dev(ranmar_gauss_state* d_g, uint64_t n_streams, 
     return RANMAR_OK;
 }
 
+int ranmar_current_device(int* device) {
+    if (!device) return fail(RANMAR_EINVAL, "ranmar: null output");
+    RB_CUDA(cudaGetDevice(device), "cudaGetDevice");
+    return RANMAR_OK;
+}
+
 int ranmar_device_status(uint32_t* flags, int clear) {
-    RB_STATUS_PTR(status);
+    const DevRes* r = nullptr;
+    if (int rc = current_res(&r)) return rc;
+    uint32_t* status = r->status;
     RB_CUDA(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     uint32_t h = 0;
     RB_CUDA(cudaMemcpy(&h, status, 4, cudaMemcpyDeviceToHost), "cudaMemcpy(status)");
@@ -818,6 +966,7 @@ int ranmar_device_status(uint32_t* flags, int clear) {
 // ------------------------------------------------------- host-buffer context
 struct ranmar_ctx {
     int device = 0;
+    uint32_t* status = nullptr;  // this context's own sticky status word
     cudaStream_t st[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     void* dbuf[2] = {nullptr, nullptr};  // per-slot output chunk
@@ -852,6 +1001,28 @@ int ctx_states(ranmar_ctx* c, uint64_t n) {
 
 constexpr size_t kChunkBytes = size_t(512) << 20;  // output bytes per pipelined chunk
 
+// Routes the status bits of the kernels a ctx_* call launches to the context's
+// own word, so concurrent users of the device's word are neither cleared nor
+// blamed, and the check needs only the context's stream, not the device.
+class StatusScope {
+  public:
+    explicit StatusScope(uint32_t* word) : prev_(g_status_override) { g_status_override = word; }
+    ~StatusScope() { g_status_override = prev_; }
+
+  private:
+    uint32_t* prev_;
+};
+
+int ctx_check_status(ranmar_ctx* c, cudaStream_t s) {
+    uint32_t h = 0;
+    RB_CUDA(cudaMemcpyAsync(&h, c->status, 4, cudaMemcpyDeviceToHost, s), "D2H status");
+    RB_CUDA(cudaStreamSynchronize(s), "sync");
+    if (h == 0) return RANMAR_OK;
+    RB_CUDA(cudaMemsetAsync(c->status, 0, 4, s), "clear status");
+    RB_CUDA(cudaStreamSynchronize(s), "sync");
+    return fail(RANMAR_ESTATE, "ranmar: a device state violated the invariants");
+}
+
 template <class T>
 int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream, T* h_out,
                  int (*gen)(ranmar_state*, uint64_t, uint64_t, T*, void*),
@@ -864,7 +1035,9 @@ int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per
         if (!host_state_ok(h_states[k]))
             return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
                                            " violates cursor/residue invariants");
-    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
     if (n == 1 && ranmar_generate_single_workspace(per_stream) > 0) {
         // one long stream: full width through substreams (ranmar_generate_single_*)
         const size_t bytes = per_stream * sizeof(T);
@@ -882,13 +1055,9 @@ int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per
         RB_CUDA(cudaMemcpyAsync(h_states, c->dstates, sizeof(ranmar_state), cudaMemcpyDeviceToHost,
                                 c->st[0]),
                 "D2H state");
-        RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
         c->h2d = sizeof(ranmar_state);
         c->d2h = bytes + sizeof(ranmar_state);
-        uint32_t flags = 0;
-        if (int rc = ranmar_device_status(&flags, 1)) return rc;
-        if (flags) return fail(RANMAR_ESTATE, "ranmar: a device state violated the invariants");
-        return RANMAR_OK;
+        return ctx_check_status(c, c->st[0]);
     }
     const size_t stream_bytes = per_stream * sizeof(T);
     uint64_t chunk = stream_bytes ? std::max<uint64_t>(1, kChunkBytes / stream_bytes) : n;
@@ -920,11 +1089,7 @@ int ctx_generate(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per
                             cudaMemcpyDeviceToHost, c->st[0]),
             "D2H states");
     c->d2h += n * sizeof(ranmar_state);
-    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
-    uint32_t flags = 0;
-    if (int rc = ranmar_device_status(&flags, 1)) return rc;
-    if (flags) return fail(RANMAR_ESTATE, "ranmar: a device state violated the invariants");
-    return RANMAR_OK;
+    return ctx_check_status(c, c->st[0]);
 }
 
 }  // namespace
@@ -936,13 +1101,25 @@ int ranmar_ctx_create(int device, ranmar_ctx** out) {
     int count = 0;
     RB_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
     if (device < 0 || device >= count) return fail(RANMAR_ECUDA, "ranmar: no such CUDA device");
-    RB_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(device), "cudaSetDevice");
     ranmar_ctx* c = new (std::nothrow) ranmar_ctx();
     if (!c) return fail(RANMAR_ENOMEM, "ranmar: out of host memory");
     c->device = device;
-    for (int i = 0; i < 2; ++i) {
-        RB_CUDA(cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking), "cudaStreamCreate");
-        RB_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    int rc = RANMAR_OK;
+    for (int i = 0; i < 2 && rc == RANMAR_OK; ++i) {
+        if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess)
+            rc = fail(RANMAR_ECUDA, "ranmar: cudaStreamCreate / cudaEventCreate failed");
+    }
+    if (rc == RANMAR_OK) rc = ranmar_device_setup(device, c->st[0]);
+    if (rc == RANMAR_OK && (cudaMalloc(&c->status, 4) != cudaSuccess ||
+                            cudaMemsetAsync(c->status, 0, 4, c->st[0]) != cudaSuccess ||
+                            cudaStreamSynchronize(c->st[0]) != cudaSuccess))
+        rc = fail(RANMAR_ECUDA, "ranmar: context status word");
+    if (rc != RANMAR_OK) {
+        ranmar_ctx_destroy(c);
+        return rc;
     }
     *out = c;
     return RANMAR_OK;
@@ -950,7 +1127,9 @@ int ranmar_ctx_create(int device, ranmar_ctx** out) {
 
 void ranmar_ctx_destroy(ranmar_ctx* c) {
     if (!c) return;
-    cudaSetDevice(c->device);
+    DeviceGuard guard;
+    guard.enter(c->device);
+    if (c->status) cudaFree(c->status);
     for (int i = 0; i < 2; ++i) {
         if (c->st[i]) cudaStreamDestroy(c->st[i]);
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
@@ -975,7 +1154,9 @@ int ranmar_ctx_make_streams(ranmar_ctx* c, uint32_t seed, const ranmar_jump_coun
     ranmar_state base;
     if (int rc = ranmar_init(seed, &base)) return rc;  // init.hpp:19-20 range check
     if (n == 0) return fail(RANMAR_EINVAL, "ranmar: need at least one stream");
-    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
     if (int rc = ctx_states(c, n)) return rc;
     if (int rc = ctx_reserve(&c->dws, &c->dws_bytes, ranmar_make_streams_workspace(n))) return rc;
     if (int rc = ranmar_make_streams_dev(&base, j, first, n, c->dstates, c->dws, c->dws_bytes,
@@ -985,8 +1166,7 @@ int ranmar_ctx_make_streams(ranmar_ctx* c, uint32_t seed, const ranmar_jump_coun
                             c->st[0]),
             "D2H states");
     c->d2h += n * sizeof(ranmar_state);
-    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
-    return RANMAR_OK;
+    return ctx_check_status(c, c->st[0]);
 }
 
 int ranmar_ctx_jump(ranmar_ctx* c, const ranmar_state* h_in, ranmar_state* h_out, uint64_t n,
@@ -999,7 +1179,9 @@ int ranmar_ctx_jump(ranmar_ctx* c, const ranmar_state* h_in, ranmar_state* h_out
         if (!host_state_ok(h_in[k]))
             return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
                                            " violates cursor/residue invariants");
-    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
     if (int rc = ctx_states(c, n)) return rc;
     if (int rc = ctx_reserve(&c->dws, &c->dws_bytes, 4096)) return rc;
     RB_CUDA(cudaMemcpyAsync(c->dstates, h_in, n * sizeof(ranmar_state), cudaMemcpyHostToDevice,
@@ -1012,8 +1194,7 @@ int ranmar_ctx_jump(ranmar_ctx* c, const ranmar_state* h_in, ranmar_state* h_out
                             c->st[0]),
             "D2H states");
     c->d2h += n * sizeof(ranmar_state);
-    RB_CUDA(cudaStreamSynchronize(c->st[0]), "sync");
-    return RANMAR_OK;
+    return ctx_check_status(c, c->st[0]);
 }
 
 int ranmar_ctx_generate_u32(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
@@ -1038,7 +1219,9 @@ int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64
         if (!host_state_ok(h_states[k]))
             return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
                                            " violates cursor/residue invariants");
-    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
     if (int rc = ctx_states(c, n)) return rc;
     const size_t need = n * (8 + 256 * 4);
     if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], need)) return rc;
@@ -1056,8 +1239,7 @@ int ranmar_ctx_consume(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64
                             s),
             "D2H states");
     c->d2h += n * (8 + 256 * 4 + sizeof(ranmar_state));
-    RB_CUDA(cudaStreamSynchronize(s), "sync");
-    return RANMAR_OK;
+    return ctx_check_status(c, s);
 }
 
 int ranmar_ctx_gaussian_stream(ranmar_ctx* c, ranmar_gauss_state* h_g, uint64_t n, uint64_t count,
@@ -1070,7 +1252,9 @@ int ranmar_ctx_gaussian_stream(ranmar_ctx* c, ranmar_gauss_state* h_g, uint64_t 
         if (!host_state_ok(h_g[k].s))
             return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
                                            " violates cursor/residue invariants");
-    RB_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
     const size_t gbytes = n * sizeof(ranmar_gauss_state), obytes = n * count * sizeof(double);
     if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], gbytes + obytes)) return rc;
     ranmar_gauss_state* dg = static_cast<ranmar_gauss_state*>(c->dbuf[0]);
@@ -1082,8 +1266,131 @@ int ranmar_ctx_gaussian_stream(ranmar_ctx* c, ranmar_gauss_state* h_g, uint64_t 
     if (obytes) RB_CUDA(cudaMemcpyAsync(h_out, dout, obytes, cudaMemcpyDeviceToHost, s), "D2H out");
     RB_CUDA(cudaMemcpyAsync(h_g, dg, gbytes, cudaMemcpyDeviceToHost, s), "D2H gauss states");
     c->d2h += gbytes + obytes;
-    RB_CUDA(cudaStreamSynchronize(s), "sync");
-    return RANMAR_OK;
+    return ctx_check_status(c, s);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Stages `k` host inputs into the context's scratch, runs `launch` on the
+// context stream with device pointers, copies `m` outputs back; synchronous.
+struct HostSpan {
+    const void* h;
+    size_t bytes;
+};
+struct HostOut {
+    void* h;
+    size_t bytes;
+};
+template <class Launch>
+int ctx_roundtrip(ranmar_ctx* c, std::initializer_list<HostSpan> in, std::initializer_list<HostOut> out,
+                  Launch launch) {
+    if (!c) return fail(RANMAR_EINVAL, "ranmar: null context");
+    c->h2d = c->d2h = 0;
+    DeviceGuard guard;
+    RB_CUDA(guard.enter(c->device), "cudaSetDevice");
+    StatusScope scope(c->status);
+    size_t total = 0;
+    for (const auto& x : in) total += align256(x.bytes);
+    for (const auto& x : out) total += align256(x.bytes);
+    if (int rc = ctx_reserve(&c->dbuf[0], &c->dbuf_bytes[0], total ? total : 256)) return rc;
+    cudaStream_t s = c->st[0];
+    char* p = static_cast<char*>(c->dbuf[0]);
+    std::vector<void*> din, dout;
+    for (const auto& x : in) {
+        if (x.bytes) RB_CUDA(cudaMemcpyAsync(p, x.h, x.bytes, cudaMemcpyHostToDevice, s), "H2D");
+        c->h2d += x.bytes;
+        din.push_back(p);
+        p += align256(x.bytes);
+    }
+    for (const auto& x : out) {
+        dout.push_back(p);
+        p += align256(x.bytes);
+    }
+    if (int rc = launch(din, dout, static_cast<void*>(s))) return rc;
+    size_t q = 0;
+    for (const auto& x : out) {
+        if (x.bytes) RB_CUDA(cudaMemcpyAsync(x.h, dout[q], x.bytes, cudaMemcpyDeviceToHost, s), "D2H");
+        c->d2h += x.bytes;
+        ++q;
+    }
+    return ctx_check_status(c, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ranmar_ctx_generate_trace(ranmar_ctx* c, ranmar_state* h_states, uint64_t n, uint64_t per_stream,
+                              uint32_t* h_u, uint32_t* h_x, uint32_t* h_v) {
+    if (n && (!h_states || (per_stream && (!h_u || !h_x || !h_v))))
+        return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    for (uint64_t k = 0; k < n; ++k)
+        if (!host_state_ok(h_states[k]))
+            return fail(RANMAR_ESTATE, "ranmar: state " + std::to_string(k) +
+                                           " violates cursor/residue invariants");
+    const size_t sb = n * sizeof(ranmar_state), ob = n * per_stream * 4;
+    return ctx_roundtrip(c, {{h_states, sb}}, {{h_u, ob}, {h_x, ob}, {h_v, ob}, {h_states, sb}},
+                         [&](std::vector<void*>& din, std::vector<void*>& dout, void* s) {
+                             ranmar_state* d = static_cast<ranmar_state*>(din[0]);
+                             if (int rc = ranmar_generate_trace_dev(d, n, per_stream,
+                                                                    static_cast<uint32_t*>(dout[0]),
+                                                                    static_cast<uint32_t*>(dout[1]),
+                                                                    static_cast<uint32_t*>(dout[2]), s))
+                                 return rc;
+                             RB_CUDA(cudaMemcpyAsync(dout[3], d, sb, cudaMemcpyDeviceToDevice,
+                                                     static_cast<cudaStream_t>(s)),
+                                     "D2D states");
+                             return static_cast<int>(RANMAR_OK);
+                         });
+}
+
+int ranmar_ctx_float_trace(ranmar_ctx* c, ranmar_float_state* h_states, uint64_t n, uint64_t per_stream,
+                           double* h_out, double* h_y, double* h_c) {
+    if (n && (!h_states || (per_stream && (!h_out || !h_y || !h_c))))
+        return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    const size_t sb = n * sizeof(ranmar_float_state), ob = n * per_stream * 8;
+    return ctx_roundtrip(c, {{h_states, sb}}, {{h_out, ob}, {h_y, ob}, {h_c, ob}, {h_states, sb}},
+                         [&](std::vector<void*>& din, std::vector<void*>& dout, void* s) {
+                             ranmar_float_state* d = static_cast<ranmar_float_state*>(din[0]);
+                             if (int rc = ranmar_generate_float_trace_dev(
+                                     d, n, per_stream, static_cast<double*>(dout[0]),
+                                     static_cast<double*>(dout[1]), static_cast<double*>(dout[2]), s))
+                                 return rc;
+                             RB_CUDA(cudaMemcpyAsync(dout[3], d, sb, cudaMemcpyDeviceToDevice,
+                                                     static_cast<cudaStream_t>(s)),
+                                     "D2D states");
+                             return static_cast<int>(RANMAR_OK);
+                         });
+}
+
+int ranmar_ctx_pow_t_mod(ranmar_ctx* c, const ranmar_jump_count* j, uint32_t* h_coeff) {
+    if (!j || !h_coeff) return fail(RANMAR_EINVAL, "ranmar: null argument");
+    return ctx_roundtrip(c, {}, {{h_coeff, 97 * 4}},
+                         [&](std::vector<void*>&, std::vector<void*>& dout, void* s) {
+                             return ranmar_pow_t_mod_dev(j, static_cast<uint32_t*>(dout[0]), s);
+                         });
+}
+
+int ranmar_ctx_poly_mul_mod(ranmar_ctx* c, const uint32_t* h_a, const uint32_t* h_b, uint32_t* h_out,
+                            uint64_t n) {
+    if (n && (!h_a || !h_b || !h_out)) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    return ctx_roundtrip(c, {{h_a, n * 97 * 4}, {h_b, n * 97 * 4}}, {{h_out, n * 97 * 4}},
+                         [&](std::vector<void*>& din, std::vector<void*>& dout, void* s) {
+                             return ranmar_poly_mul_mod_dev(static_cast<uint32_t*>(din[0]),
+                                                            static_cast<uint32_t*>(din[1]),
+                                                            static_cast<uint32_t*>(dout[0]), n, s);
+                         });
+}
+
+int ranmar_ctx_poly_reduce(ranmar_ctx* c, const uint32_t* h_raw, uint32_t* h_out, uint64_t n) {
+    if (n && (!h_raw || !h_out)) return fail(RANMAR_EINVAL, "ranmar: null host buffer");
+    return ctx_roundtrip(c, {{h_raw, n * 193 * 4}}, {{h_out, n * 97 * 4}},
+                         [&](std::vector<void*>& din, std::vector<void*>& dout, void* s) {
+                             return ranmar_poly_reduce_dev(static_cast<uint32_t*>(din[0]),
+                                                           static_cast<uint32_t*>(dout[0]), n, s);
+                         });
 }
 
 }  // extern "C"

@@ -36,6 +36,10 @@ int main(void) {
     CHECK(cudaMalloc((void**)&d_states, n * sizeof(ranmar_state)) == cudaSuccess);
     CHECK(cudaMalloc((void**)&d_out, n * per * sizeof(uint32_t)) == cudaSuccess);
     CHECK(cudaMalloc(&d_ws, ws) == cudaSuccess);
+    /* the _dev entry points never allocate: the device's one-time resources
+     * come from ranmar_device_setup (RANMAR_ESTATE until then) */
+    CHECK(ranmar_make_streams_dev(&base, &J, 0, n, d_states, d_ws, ws, NULL) == RANMAR_ESTATE);
+    CHECK(ranmar_device_setup(0, NULL) == RANMAR_OK);
     CHECK(ranmar_make_streams_dev(&base, &J, 0, n, d_states, d_ws, ws, NULL) == RANMAR_OK);
     CHECK(ranmar_generate_u32_dev(d_states, n, per, d_out, NULL) == RANMAR_OK);
     uint32_t* h = (uint32_t*)malloc(n * per * sizeof(uint32_t));

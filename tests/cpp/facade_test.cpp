@@ -100,6 +100,65 @@ int main() {
         CHECK(same.state() == r.state());
         CHECK(throws_invalid([] { RanMars bad(900000001u); }));
     }
+    // scalar step() / next_f64() on the caller's state (core.hpp:54-72): the
+    // reference's frozen outputs, copies of a state continue identically, the
+    // state after n calls equals the bulk path's, and a modified state is
+    // noticed (test_core.cpp:118-126)
+    {
+        auto s = init(12345);
+        const std::uint32_t first[10] = {1905444, 14595391, 174918,   4925251,  346329,
+                                         1286474, 5077740,  10808695, 10092480, 6540075};
+        for (auto e : first) {
+            auto probe = s;  // demo/basic_usage.cpp's peek
+            CHECK(step(probe) == e);
+            CHECK(next_f64(s) == e * 0x1p-24);
+            CHECK(probe == s);
+        }
+        for (int n = 10; n < 999999; ++n) step(s);
+        CHECK(step(s) == 7864902u);  // output #1,000,000
+        std::vector<RanmarState> bulk(1, init(12345));
+        generate_u32(bulk, 1000000);
+        CHECK(bulk[0] == s);
+        auto t = init(12345);
+        step(t);
+        t.fib.lane[5] ^= 1;  // a modified state must not be served from the cache
+        auto t2 = t;
+        std::vector<RanmarState> tb(1, t2);
+        const auto exp = generate_u32(tb, 3);
+        for (int n = 0; n < 3; ++n) CHECK(step(t) == exp[n]);
+        CHECK(t == tb[0]);
+    }
+    // reference::step_float on the caller's FloatState (float_ranmar.hpp:33-46)
+    // equals value_of(step()) and keeps the state isomorphic
+    {
+        auto s = init(900000000u);
+        auto f = reference::init_float(900000000u);
+        for (int n = 0; n < 300000; ++n) CHECK(value_of(step(s)) == reference::step_float(f));
+        for (int k = 0; k < long_lag; ++k) CHECK(reference::to_u24(f.x[k]) == s.fib.lane[k]);
+        CHECK(f.i == s.fib.i && f.j == s.fib.j && reference::to_u24(f.c) == s.arith.v);
+    }
+    // poly on the GPU (polyring.hpp): t has order exactly 2^23 (2^97 - 1) mod
+    // phi over Z/2^24 -- the period the facade reduces jump counts by
+    {
+        using poly::PolyMod;
+        const JumpCount ord = (JumpCount(1) << 23) * ((JumpCount(1) << 97) - 1);
+        CHECK(poly::pow_t_mod<24>(ord) == PolyMod<24>::one());
+        CHECK(!(poly::pow_t_mod<24>(ord / 2) == PolyMod<24>::one()));
+        CHECK(!(poly::pow_t_mod<24>((JumpCount(1) << 97) - 1) == PolyMod<24>::one()));
+        CHECK(poly::pow_t_mod<24>(JumpCount(97)).coeff[64] == word_mask);  // t^97 = 1 - t^64
+        const auto a = poly::pow_t_mod<24>(JumpCount(123456789)), b = poly::pow_t_mod<24>(JumpCount(987654));
+        CHECK(poly::mul_mod(a, b) == poly::pow_t_mod<24>(JumpCount(123456789 + 987654)));
+        CHECK(poly::mul_by_t(a) == poly::pow_t_mod<24>(JumpCount(123456790)));
+        std::vector<std::uint32_t> raw(193, 0);
+        raw[192] = 1;  // t^192 mod phi = t^95 * t^97 = t^95 - t^159 = ...
+        CHECK(poly::reduce_trinomial<24>(raw) == poly::pow_t_mod<24>(JumpCount(192)));
+        // huge jumps reduce by the period: J and J + period give the same state
+        const auto s = init(31337);
+        const JumpCount huge = parse_jump_count("2^100000+1");
+        CHECK(jump_state(s, huge) == jump_state(s, huge + detail::state_period() * JumpCount(3)));
+        CHECK(jump_state(s, ord * JumpCount(arith_mod)) == jump_state(s, JumpCount(0)));
+        CHECK(canonicalize(jump_state(s, JumpCount(1)).fib) == apply_companion(canonicalize(s.fib)));
+    }
     // serialize.hpp round trip
     {
         const auto s = jump_state(init(4711), JumpCount(1) << 100);

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
-    assert rb.lib().ranmar_abi_version() == 1
+    assert rb.lib().ranmar_abi_version() == 2
 
 
 def test_sm100a_cubin_present():

@@ -302,16 +302,39 @@ def test_gaussian_within_one_ulp(oracle):
     d = ulp_diff(out.reshape(-1), exp.reshape(-1))
     print(f"gaussian max ulp {d.max()}, differing {np.count_nonzero(d)} of {d.size}")
     assert d.max() <= 1  # north-star tolerance
-    assert d.max() == 0  # and the shared log convention makes it bit-exact
+    assert d.max() == 0  # correctly rounded log on both sides: bit-exact
     og2 = np.zeros(n, GAUSS_DTYPE)
     og2["s"] = rb.states_to_host(states)
-    libm = oracle.gaussian_fill(og2, per, steps, libm_log=True)
+    libm, flags = oracle.gaussian_fill(og2, per, steps, libm_log=True, with_flags=True)
     d2 = ulp_diff(out.reshape(-1), libm.reshape(-1))
-    print(f"vs a glibc-log() variant of the convention: max ulp {d2.max()}")
-    assert d2.max() <= 4
+    print(f"vs the glibc-log() form: max ulp {d2.max()}, differing {np.count_nonzero(d2)}")
+    # deviates move only where glibc's own log(rsq) is misrounded
+    # (glibc's 1-ulp log error grows to at most 3 ulp through /rsq, sqrt and v*fac)
+    assert (d2[flags.reshape(-1) == 0] == 0).all() and d2.max() <= 3
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
     assert gh["s"].tobytes() == og["s"].tobytes()
     assert (gh["has_saved"] == og["has_saved"]).all()
+
+
+def test_crlog_sweep_matches_oracle(oracle):
+    # the device's correctly rounded log on a slice of gaussian()'s domain:
+    # every input the fast phase leaves undecided is decided by the accurate
+    # phase, both phases agree where the fast one decides (mode 1), and the
+    # undecided inputs equal the oracle's list (the same IEEE sequence)
+    import random
+    rng = random.Random(11)
+    for _ in range(4):
+        s0 = rng.randrange(1, 2**46 - 2**27)
+        nf, nacc, nmis, fails = rb.crlog_sweep(s0, 2**27, mode=1)
+        assert nacc == 0 and nmis == 0
+        n2, exp = oracle.crlog_scan(s0, 2**27)
+        assert nf == n2 and fails == sorted(exp)
+    # a long slice in mode 0 (the mode of the full sweep, tools/crlog_sweep.py)
+    nf, nacc, nmis, fails = rb.crlog_sweep(2**45, 2**36, mode=0)
+    assert nacc == 0 and nf == len(fails)
+    for s in fails[:200]:
+        y, ok = oracle.crlog_accurate(s * 2.0**-46)
+        assert ok
 
 
 def test_fp64_fast_paths_match_library():

@@ -245,6 +245,7 @@ int run_bench(const std::map<std::string, std::string>& o) {
     ranmar_float_state* df = nullptr;
     void* dout = nullptr;
     const std::uint64_t n_out = count ? count : 1;
+    detail::check(ranmar_device_setup(0, nullptr));
     CUDA_OK(cudaMalloc(&ds, sizeof(ranmar_state)));
     CUDA_OK(cudaMalloc(&df, sizeof(ranmar_float_state)));
     CUDA_OK(cudaMalloc(&dout, n_out * sizeof(double)));
@@ -317,6 +318,7 @@ int run_selftest() {
             detail::check(ranmar_init_float(seed, &f));
             ranmar_float_state* df = nullptr;
             double* dout = nullptr;
+            detail::check(ranmar_device_setup(0, nullptr));
             CUDA_OK(cudaMalloc(&df, sizeof f));
             CUDA_OK(cudaMalloc(&dout, 100000 * sizeof(double)));
             CUDA_OK(cudaMemcpy(df, &f, sizeof f, cudaMemcpyHostToDevice));
