@@ -131,7 +131,8 @@ int ranmar_make_streams_from_dev(const ranmar_state* d_base, const ranmar_jump_c
                                  void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* d_out[k] = ranmar::jump_state(d_in[k], J) for k < n (jump.hpp:90-95).
- * d_in == d_out is allowed. */
+ * d_in == d_out is allowed. A state violating the invariants raises the
+ * status bit (its output is unspecified; nothing is read outside it). */
 int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
                     const ranmar_jump_count* j, void* d_workspace, size_t workspace_bytes,
                     void* stream);
@@ -241,7 +242,8 @@ int ranmar_gaussian_stream_f64_dev(ranmar_gauss_state* d_g, uint64_t n_streams, 
 /* Device-side persistence (bulk serialize.hpp:21-136). to_text: d_text gets
  * the concatenated "ranmar24 v1" texts of n device states, d_offsets[0..n]
  * their start offsets (d_offsets[n] = total bytes); text_cap must be at least
- * ranmar_to_text_bound(n). from_text: parses texts [d_offsets[k],
+ * ranmar_to_text_bound(n). A state violating the invariants (cursors, v,
+ * 24-bit lanes) gets an empty text and raises the status bit. from_text: parses texts [d_offsets[k],
  * d_offsets[k+1]) with the reference's strict rules; d_err[k] = 0 or the
  * 1-based line of the first error (where from_text throws invalid_argument),
  * d_states[k] written only on success. */
@@ -261,6 +263,12 @@ int ranmar_device_status(uint32_t* flags, int clear);
 /* Number of kernels this library has launched in this process (all devices);
  * diagnostic evidence for benchmarks ("gpu_launches"). */
 uint64_t ranmar_kernel_launches(void);
+
+/* The state isomorphism of float_ranmar.hpp:3-8 on the device: d_out[k] =
+ * the float state of d_states[k] (x = lane / 2^24, c = v / 2^24, same
+ * cursors), so float streams can start from integer jumps. */
+int ranmar_float_from_states_dev(const ranmar_state* d_states, uint64_t n, ranmar_float_state* d_out,
+                                 void* stream);
 
 /* Per-step trace for the scalar step()/next_f64() of the C++ facade: for
  * step n of stream k, at index k * per_stream + n: d_u = the output

@@ -44,6 +44,7 @@
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <initializer_list>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -498,12 +499,15 @@ inline std::uint32_t step(RanmarState& s) {
                                                 out.x.data(), out.v.data()));
     });
     const std::size_t p = ent.pos++;
-    FibState& f = s.fib;
-    f.lane[f.i] = ent.w.x[p];
-    f.i = (f.i == 0) ? long_lag - 1 : f.i - 1;
-    f.j = (f.j == 0) ? long_lag - 1 : f.j - 1;
-    s.arith.v = ent.w.v[p];
-    ent.cur = s;
+    // the same word updates on the caller's state and on the cache's copy of it
+    // (equal before the call), so they stay equal without a 400-byte copy
+    for (RanmarState* x : {&s, &ent.cur}) {
+        FibState& f = x->fib;
+        f.lane[f.i] = ent.w.x[p];
+        f.i = (f.i == 0) ? long_lag - 1 : f.i - 1;
+        f.j = (f.j == 0) ? long_lag - 1 : f.j - 1;
+        x->arith.v = ent.w.v[p];
+    }
     return ent.w.u[p];
 }
 
@@ -719,11 +723,12 @@ inline double step_float(FloatState& s) {
                                                      o.out.data(), o.y.data(), o.c.data()));
     });
     const std::size_t p = ent.pos++;
-    s.x[s.i] = ent.w.y[p];
-    s.i = (s.i == 0) ? long_lag - 1 : s.i - 1;
-    s.j = (s.j == 0) ? long_lag - 1 : s.j - 1;
-    s.c = ent.w.c[p];
-    ent.cur = s;
+    for (FloatState* x : {&s, &ent.cur}) {
+        x->x[x->i] = ent.w.y[p];
+        x->i = (x->i == 0) ? long_lag - 1 : x->i - 1;
+        x->j = (x->j == 0) ? long_lag - 1 : x->j - 1;
+        x->c = ent.w.c[p];
+    }
     return ent.w.out[p];
 }
 

@@ -512,9 +512,10 @@ double or_crlog_ex(double x, int* fast) {
     const double t1 = crlog_t12[2 * i], t2 = crlog_t12[2 * i + 1];
     const double ah = k1 + t1;
     const double al = t1 - (ah - k1);
-    /* + log1p head: TwoSum */
-    double bh, bl;
-    or_two_sum(ah, s1, &bh, &bl);
+    /* + log1p head: Fast2Sum, exact because |ah| >= |s1| whenever ah != 0
+     * (|s1| < 2^-7; a nonzero ah is at least |T_i| >= 2^-6.4 or |e ln2| - 0.35) */
+    const double bh = ah + s1;
+    const double bl = s1 - (bh - ah);
     double lo = fma(ed, CRLOG_LN2_MID, t2) + al;
     lo = lo + bl;
     lo = lo + lo1;

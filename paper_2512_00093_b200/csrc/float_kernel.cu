@@ -100,7 +100,31 @@ __global__ void __launch_bounds__(32 * kFWarps)
     }
 }
 
+// The reference's state isomorphism (float_ranmar.hpp:3-8, 84-95) on the
+// device: integer state -> float state, x[k] = lane[k] / 2^24, c = v / 2^24,
+// same cursors; exact. A warp per state.
+__global__ void float_from_states_kernel(const ranmar_state* __restrict__ in, uint64_t n,
+                                         ranmar_float_state* __restrict__ out) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (k >= n) return;
+    const int l = threadIdx.x & 31;
+    for (int q = l; q < 97; q += 32) out[k].x[q] = static_cast<double>(in[k].lane[q] & kMask) * 0x1p-24;
+    if (l == 0) {
+        out[k].c = static_cast<double>(in[k].v) * 0x1p-24;
+        out[k].i = in[k].i;
+        out[k].j = in[k].j;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_float_from_states(const ranmar_state* d_in, uint64_t n, ranmar_float_state* d_out,
+                                     cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    count_launch();
+    float_from_states_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, stream>>>(d_in, n, d_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_float_gen(ranmar_float_state* d_states, uint64_t n_streams, uint64_t per_stream,
                              double* d_out, double* d_y, double* d_c, uint32_t* status,

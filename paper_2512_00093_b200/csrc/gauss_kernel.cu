@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kGT)
             v2[k] = polar_v(b[k]);
         }
 #pragma unroll
-        for (int k = 0; k < K; ++k) fac[k] = polar_fac(v1[k], v2[k]);
+        for (int k = 0; k < K; ++k) fac[k] = polar_fac(a[k], b[k]);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             put(__dmul_rn(v2[k], fac[k]));
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kGT)
         uint32_t u0, u1;
         accept(u0, u1);
         const double v1 = polar_v(u0), v2 = polar_v(u1);
-        const double fac = polar_fac(v1, v2);
+        const double fac = polar_fac(u0, u1);
         saved = __dmul_rn(v1, fac);
         put(__dmul_rn(v2, fac));
         if (q + 1 < G) {

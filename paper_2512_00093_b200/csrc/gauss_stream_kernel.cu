@@ -127,9 +127,10 @@ __global__ void __launch_bounds__(32 * kSW)
         uint32_t at = 0;
         if (static_cast<uint32_t>(l) < cnt) {
             const uint32_t slot = (qhead + l) & (kQCap - 1);
-            const double v1 = polar_v(qu1[w][slot]), v2 = polar_v(qu2[w][slot]);
+            const uint32_t u1 = qu1[w][slot], u2 = qu2[w][slot];
+            const double v1 = polar_v(u1), v2 = polar_v(u2);
             at = qat[w][slot];
-            const double fac = polar_fac(v1, v2);
+            const double fac = polar_fac(u1, u2);
             g1 = __dmul_rn(v2, fac);
             g2 = __dmul_rn(v1, fac);
             const uint64_t qa = q + 2 * static_cast<uint64_t>(l);

@@ -342,7 +342,7 @@ constexpr size_t kA2Smem = (size_t(kA2Items) * kA2Stride + 128 + 2 * kA2Items) *
 
 __global__ void __launch_bounds__(kA2Threads, 3)
     apply2_kernel(const ranmar_state* in, ranmar_state* out, uint64_t n,
-                  const uint32_t* __restrict__ P, uint32_t dec) {
+                  const uint32_t* __restrict__ P, uint32_t dec, uint32_t* status) {
     extern __shared__ uint32_t sm[];
     uint32_t* W = sm;                                   // [128][193]
     uint32_t* p = W + kA2Items * kA2Stride;             // [128] (97 used)
@@ -361,14 +361,21 @@ __global__ void __launch_bounds__(kA2Threads, 3)
 #pragma unroll 2
         for (int it = g; it < items; it += kA2Threads / 32) {
             const ranmar_state* src = in + k0 + it;
-            const int i0 = src->i;
+            // a state violating the invariants raises the status bit; its
+            // cursor is clamped so the reads stay inside the record
+            const bool ok = state_ok(src->i, src->j, src->v);
+            const int i0 = ok ? src->i : 96;
             uint32_t* Wi = W + it * kA2Stride;
+            bool bad = !ok;
 #pragma unroll
             for (int kk = l; kk < kPolyN; kk += 32) {
                 int q = i0 - kk;
                 q += q < 0 ? 97 : 0;
-                Wi[kk] = src->lane[q];
+                const uint32_t x = src->lane[q];
+                bad |= x > kMask;
+                Wi[kk] = x;
             }
+            if (__any_sync(0xffffffffu, bad) && l == 0) atomicOr(status, kStatusBadState);
         }
     }
     __syncthreads();
@@ -789,12 +796,12 @@ cudaError_t configure_jump_kernels() {
 }
 
 cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, const uint32_t* P,
-                         uint32_t dec, cudaStream_t stream) {
+                         uint32_t dec, uint32_t* status, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
     count_launch();
     apply2_kernel<<<static_cast<unsigned>((n + kA2Items - 1) / kA2Items), kA2Threads, kA2Smem,
-                    stream>>>(in, out, n, P, dec);
+                    stream>>>(in, out, n, P, dec, status);
     return cudaGetLastError();
 }
 

@@ -61,7 +61,7 @@ __device__ __forceinline__ double gauss_next(InPlace& st, double& saved, bool& h
         if (s > 0 && s < (int64_t(1) << 46)) break;
     }
     const double v1 = polar_v(u0), v2 = polar_v(u1);
-    const double fac = polar_fac(v1, v2);
+    const double fac = polar_fac(u0, u1);
     saved = __dmul_rn(v1, fac);
     has = true;
     return __dmul_rn(v2, fac);

@@ -38,10 +38,12 @@ cudaError_t launch_float_gen(ranmar_float_state*, uint64_t, uint64_t, double*, d
                              uint32_t*, cudaStream_t);
 cudaError_t launch_generate_trace(ranmar_state*, uint64_t, uint64_t, uint32_t*, uint32_t*, uint32_t*,
                                   uint32_t*, cudaStream_t);
+cudaError_t launch_float_from_states(const ranmar_state*, uint64_t, ranmar_float_state*, cudaStream_t);
 cudaError_t launch_poly(int, const uint32_t*, const uint32_t*, uint32_t*, uint64_t, cudaStream_t);
 uint64_t text_bound(uint64_t);
 size_t text_workspace(uint64_t);
-cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void*, cudaStream_t);
+cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void*, uint32_t*,
+                           cudaStream_t);
 cudaError_t launch_from_text(const char*, const uint64_t*, uint64_t, ranmar_state*, int32_t*,
                              cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
@@ -64,7 +66,7 @@ cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*
                              const uint32_t*, cudaStream_t);
 cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
-                         cudaStream_t);
+                         uint32_t*, cudaStream_t);
 cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
                          uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
@@ -531,7 +533,9 @@ int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
     int rc = ranmar_pow_t_mod_dev(j, P, stream);
     if (rc) return rc;
     const uint32_t dec = arith_dec(mod_u32(from_abi(j), kMod));
-    RB_CUDA(rb::launch_apply(d_in, d_out, n, P, dec, s), "apply_kernel launch");
+    uint32_t* status = nullptr;
+    if (int rc2 = device_status_ptr(&status, nullptr)) return rc2;
+    RB_CUDA(rb::launch_apply(d_in, d_out, n, P, dec, status, s), "apply_kernel launch");
     return RANMAR_OK;
 }
 
@@ -609,7 +613,7 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     const ranmar_state* a0 = dbase;
     if (first > 0) {
         const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(first % kMod, jm, kMod)));
-        RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, s), "apply_kernel launch");
+        RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, status, s), "apply_kernel launch");
         a0 = A0;
     }
     // Levels L-1 .. 1 of the base-128 tree (level 1 writes the anchors'
@@ -879,6 +883,14 @@ int ranmar_generate_float_trace_dev(ranmar_float_state* d_states, uint64_t n_str
     return RANMAR_OK;
 }
 
+int ranmar_float_from_states_dev(const ranmar_state* d_states, uint64_t n, ranmar_float_state* d_out,
+                                 void* stream) {
+    if (n && (!d_states || !d_out)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_CUDA(rb::launch_float_from_states(d_states, n, d_out, static_cast<cudaStream_t>(stream)),
+            "float_from_states_kernel launch");
+    return RANMAR_OK;
+}
+
 int ranmar_generate_trace_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
                               uint32_t* d_u, uint32_t* d_x, uint32_t* d_v, void* stream) {
     if (n_streams && per_stream && (!d_states || !d_u || !d_x || !d_v))
@@ -918,7 +930,9 @@ int ranmar_to_text_dev(const ranmar_state* d_states, uint64_t n, char* d_text, u
     if (!d_states || !d_text || !d_offsets || !d_ws) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
     if (text_cap < rb::text_bound(n)) return fail(RANMAR_ENOMEM, "ranmar: text buffer below ranmar_to_text_bound(n)");
     if (ws_bytes < rb::text_workspace(n)) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");
-    RB_CUDA(rb::launch_to_text(d_states, n, d_text, d_offsets, d_ws, static_cast<cudaStream_t>(stream)),
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_to_text(d_states, n, d_text, d_offsets, d_ws, status,
+                               static_cast<cudaStream_t>(stream)),
             "to_text kernels launch");
     return RANMAR_OK;
 }

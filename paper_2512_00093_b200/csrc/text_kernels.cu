@@ -88,13 +88,25 @@ __device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* 
     *p = '\n';
 }
 
-// warp per state (coalesced lane reads): the exact byte length of its text
+// warp per state (coalesced lane reads): the exact byte length of its text.
+// A state violating the reference's invariants (cursors, v, 24-bit lanes;
+// core.hpp:29-49) raises the status bit and gets an EMPTY text (length 0), so
+// text_bound() holds and no kernel writes past the caller's buffer.
 __global__ void text_len_kernel(const ranmar_state* __restrict__ st, uint64_t n,
-                                uint64_t* __restrict__ len) {
+                                uint64_t* __restrict__ len, uint32_t* status) {
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int l = threadIdx.x & 31;
     if (k >= n) return;
     const ranmar_state& s = st[k];
+    bool bad = l == 0 && !state_ok(s.i, s.j, s.v);
+    for (int q = l; q < 97; q += 32) bad |= s.lane[q] > kMask;
+    if (__any_sync(0xffffffffu, bad)) {
+        if (l == 0) {
+            len[k] = 0;
+            atomicOr(status, kStatusBadState);
+        }
+        return;
+    }
     uint32_t L = 0;
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(32 * kTTStates)
     const uint64_t kend = k0 + kTTStates < n ? k0 + kTTStates : n;
     const uint64_t g0 = off[k0], g1 = off[kend];
     const uint32_t shift = static_cast<uint32_t>(g0 & 15);
-    if (k < n) {
+    if (k < n && off[k + 1] != off[k]) {  // (invalid states have empty texts)
         const ranmar_state& s = st[k];
         char* base = stage + shift + (off[k] - g0);
         uint32_t before = 0;  // bytes of the lines of previous passes
@@ -442,7 +454,7 @@ size_t text_workspace(uint64_t n) {
 // Offsets d_off[0..n] (d_off[n] = total bytes) and the concatenated texts;
 // chunks of 2^20 states, each continuing where the previous one ended.
 cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_text,
-                           uint64_t* d_off, void* d_ws, cudaStream_t stream) {
+                           uint64_t* d_off, void* d_ws, uint32_t* status, cudaStream_t stream) {
     for (uint64_t c0 = 0; c0 < n; c0 += kTextChunk) {
         const uint64_t m = n - c0 < kTextChunk ? n - c0 : kTextChunk;
         const uint64_t blocks = (m + kScanT - 1) / kScanT;
@@ -455,7 +467,7 @@ cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_tex
         uint64_t* base_copy = boff + blocks;
         count_launch(3);
         text_len_kernel<<<static_cast<unsigned>((m + 7) / 8), 256, 0, stream>>>(d_states + c0, m,
-                                                                                len);
+                                                                                len, status);
         if (base) {
             count_launch();
             copy_u64_kernel<<<1, 1, 0, stream>>>(base_copy, base);

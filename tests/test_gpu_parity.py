@@ -413,6 +413,41 @@ def test_bad_state_is_flagged(oracle):
     assert rb.device_status(clear=True) & 1
 
 
+def test_invalid_device_states_are_flagged_not_overrun(oracle):
+    # states with unmasked lanes, a huge v or bad cursors must not
+    # make the text kernels write past text_bound(n) or the jump kernels read
+    # outside the record; each raises the status bit instead
+    good = oracle.make_streams(oracle.init(5), 2**40, 6)
+    bad = good.copy()
+    bad[1]["lane"][7] = 0xFFFFFFFF
+    bad[2]["v"] = 0xFFFFFFFF
+    bad[3]["i"], bad[3]["j"] = 1 << 30, 5
+    bad[4]["i"] = -7
+    d = rb.states_to_device(bad)
+    text, off = rb.to_text_dev(d)
+    torch.cuda.synchronize()
+    assert rb.device_status(clear=True) & 1
+    o = off.cpu().numpy()
+    assert int(o[-1]) <= text.numel()
+    lens = np.diff(o)
+    assert (lens[1:5] == 0).all() and lens[0] > 0 and lens[5] > 0
+    texts = rb.texts_to_host(text, off)
+    assert texts[0] == oracle.to_text(good[0:1]) and texts[5] == oracle.to_text(good[5:6])
+    for k in (1, 2, 3, 4):
+        rb.jump_dev(d[k:k + 1], 2**70)
+        torch.cuda.synchronize()
+        assert rb.device_status(clear=True) & 1, k
+    one = d[3:4].clone()
+    rb.generate_single(one, 50000, "u32")  # device-resident base: flagged, not trusted
+    torch.cuda.synchronize()
+    assert rb.device_status(clear=True) & 1
+    assert torch.equal(one, d[3:4])  # an invalid state is left untouched
+    ctx = rb.Context()
+    with pytest.raises(rb.RanmarError):
+        ctx.generate(bad[1:2].copy(), 10, "u32")  # host path: RANMAR_ESTATE (lanes > 2^24 - 1)
+    ctx.close()
+
+
 def test_host_buffer_context(oracle):
     ctx = rb.Context(0)
     ss = ctx.make_streams(12345, 2**40, 300)
