@@ -32,6 +32,7 @@
 //                         extensions, 4 x 8 register tiles, results stored
 //                         from registers as 16-B vectors.
 #include <cstdint>
+#include <cstdlib>
 
 #include "ranmar_device.cuh"
 
@@ -742,6 +743,288 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
     }
 }
 
+// ---- make_streams bulk on the TENSOR CORES (tcgen05.mma kind::i8).
+// The same product as bulk_kernel, C[r][m] = sum_j T[r][j] w_h[j + m] mod 2^24
+// (r < 128 offsets, m < 97 state words, j < 97), computed EXACTLY from 8-bit
+// limbs: with T = T0 + 2^8 T1 + 2^16 T2 and W = W0 + 2^8 W1 + 2^16 W2 (u8),
+//   C = D0 + 2^8 D1 + 2^16 D2 mod 2^24,  D0 = T0 W0,  D1 = T0 W1 + T1 W0,
+//   D2 = T0 W2 + T1 W1 + T2 W0,
+// six u8 x u8 -> s32 GEMMs of 128 x 112 x 128 (K padded with zero T limbs,
+// N = 112 >= 97) accumulated in TMEM (D0, D1, D2 = 336 columns); the partial
+// sums stay below 3 * 97 * 255^2 < 2^25, so the s32 accumulators are exact and
+// the only reduction is the final mask, as in the reference's 64-bit
+// accumulation (polyring.hpp:88-96). The Hankel operand W[m][k] = w[m + k] is
+// never materialised: in the canonical K-major no-swizzle layout a core
+// matrix is 8 rows x 16 bytes at a 16-byte row stride, so storing 16 shifted
+// copies of each limb plane interleaved, S[(b * 16 + s) * 16 + e] =
+// limb(w[16 b + s + e]), makes row m / K-chunk c start at
+// ((m / 16 + c) * 16 + m % 16) * 16: leading-byte offset 256 (K) and
+// stride-byte offset 128 (N) describe the whole matrix (tools/micro/tc_i8.cu).
+// A CTA per SM (128 threads) runs a software pipeline over its anchors h:
+// the 112 output columns are split into halves (N = 64 and N = 48, each
+// with its own D0/D1/D2 in TMEM: 192 + 144 of the 512 columns), so while the
+// threads read half A of anchor h from TMEM (tcgen05.ld), combine it and
+// write state records to shared memory, the tensor core already computes
+// half A of the next anchor, and likewise for half B; the W planes of the
+// next anchor are built (and its w prefetched from HBM two anchors ahead)
+// before that. The CTA's 128 consecutive records (51 KB) leave as ONE TMA
+// bulk store (cp.async.bulk) from a double-buffered staging area.
+constexpr int kTcThreads = 128;
+constexpr int kTcNA = 64, kTcNB = 48;             // column halves (m < 64, 64 <= m < 112)
+constexpr uint32_t kTcAPlane = 16384;             // 8 K-chunks x 16 row groups x 128 B
+constexpr uint32_t kTcBPlane = 3584;              // 14 blocks x 16 shifts x 16 B
+constexpr uint32_t kTcOffB = 3 * kTcAPlane;                 // 2 buffers x 3 planes
+constexpr uint32_t kTcOffW = kTcOffB + 2 * 3 * kTcBPlane;   // 240 words of w
+constexpr uint32_t kTcOffOut = kTcOffW + 1024;              // 2 x 128 records x 400 B
+constexpr uint32_t kTcOut = 128 * 400;
+constexpr uint32_t kTcSmem = kTcOffOut + 2 * kTcOut;        // 172 KB: one CTA per SM
+static_assert(kTcSmem <= 227 * 1024, "tensor-core bulk smem");
+
+struct BulkTcArgs {
+    const uint32_t* W1;   // anchors' extensions, H x kWAnchor
+    uint64_t H;
+    const uint32_t* Tt;   // [97][128]
+    ranmar_state* out;    // streams [first, first + n)
+    uint64_t first, n;
+    uint32_t jm;
+    const ranmar_state* base;
+};
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (static_cast<uint64_t>(1) << 46);
+}
+
+// byte a of each of w0..w3 packed little-endian (the limb a of four coefficients)
+__device__ __forceinline__ uint32_t limb4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t a) {
+    const uint32_t sel = a | ((a + 4) << 4);
+    return __byte_perm(__byte_perm(w0, w1, sel), __byte_perm(w2, w3, sel), 0x5410);
+}
+
+// The 24 MMAs of one column half: D0 += T0 W0; D1 += T0 W1 + T1 W0;
+// D2 += T0 W2 + T1 W1 + T2 W0 (K = 128 in 4 steps), then a commit to `bar`.
+// dA / dB: descriptors of limb plane 0 at K-step 0; planes and K steps are
+// offsets added to the 14-bit start-address field (addresses < 256 KB, no carry).
+template <int N>
+__device__ __forceinline__ void tc_issue_half(uint64_t dA, uint64_t dB, uint32_t tmem, uint32_t bar) {
+    constexpr uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (8u << 24);
+    constexpr uint32_t ta[6] = {0, 0, 1, 0, 1, 2}, tb[6] = {0, 1, 0, 2, 1, 0}, td[6] = {0, 1, 1, 2, 2, 2};
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t da = dA + ((ta[p] * kTcAPlane + ks * 4096) >> 4);
+            const uint64_t db = dB + ((tb[p] * kTcBPlane + ks * 512) >> 4);
+            if ((p == 0 || p == 1 || p == 3) && ks == 0) {  // first product of an accumulator
+                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;" ::"r"(tmem + td[p] * N),
+                             "l"(da), "l"(db), "r"(idesc)
+                             : "memory");
+            } else {
+                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(tmem + td[p] * N),
+                             "l"(da), "l"(db), "r"(idesc)
+                             : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+// Columns [c0, c0 + NC) of this thread's row: (D0 + 2^8 D1 + 2^16 D2) & mask.
+template <int NC, int N>
+__device__ __forceinline__ void tc_read_half(uint32_t trow, uint32_t (&val)[NC]) {
+#pragma unroll
+    for (int c0 = 0; c0 < NC; c0 += 16) {
+        uint32_t d[3][16];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(d[a][0]), "=r"(d[a][1]), "=r"(d[a][2]), "=r"(d[a][3]), "=r"(d[a][4]), "=r"(d[a][5]),
+                  "=r"(d[a][6]), "=r"(d[a][7]), "=r"(d[a][8]), "=r"(d[a][9]), "=r"(d[a][10]), "=r"(d[a][11]),
+                  "=r"(d[a][12]), "=r"(d[a][13]), "=r"(d[a][14]), "=r"(d[a][15])
+                : "r"(trow + a * N + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q) val[c0 + q] = (d[0][q] + (d[1][q] << 8) + (d[2][q] << 16)) & kMask;
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_constant__ BulkTcArgs args) {
+    extern __shared__ __align__(1024) uint32_t tc_smem[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>(tc_smem);
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t bars[2];  // half A, half B MMA completion
+    const int t = threadIdx.x;
+    const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    uint32_t* sw = reinterpret_cast<uint32_t*>(sm + kTcOffW);
+    const uint64_t G = gridDim.x;
+
+    // A planes (T limbs), once per CTA: row r, K-chunk c -> (c * 16 + r / 8) * 128 + (r % 8) * 16
+    for (int x = t; x < 128 * 8; x += kTcThreads) {
+        const int r = x & 127, c = x >> 7;  // consecutive threads: consecutive rows (coalesced Tt reads)
+        uint32_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int k = 16 * c + e;
+            v[e] = k < kPolyN ? args.Tt[k * kRows + r] : 0u;
+        }
+        const uint32_t off = static_cast<uint32_t>((c * 16 + (r >> 3)) * 128 + (r & 7) * 16);
+#pragma unroll
+        for (uint32_t a = 0; a < 3; ++a)
+            *reinterpret_cast<uint4*>(sm + a * kTcAPlane + off) =
+                make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
+                           limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
+    }
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    const uint32_t barA = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]));
+    const uint32_t barB = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]));
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barA) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barB) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+    // W planes of anchor hh into buffer `buf` from sw: chunk (b, s) of plane a =
+    // limb_a(w[16 b + s .. 16 b + s + 15])
+    auto build_w = [&](int buf) {
+        for (int x = t; x < 14 * 16; x += kTcThreads) {
+            const int o = 16 * (x >> 4) + (x & 15);
+            uint32_t v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = sw[o + e];
+#pragma unroll
+            for (uint32_t a = 0; a < 3; ++a)
+                *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * x) =
+                    make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
+                               limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
+        }
+    };
+    // this thread's two words of an anchor's extension (zero past 193)
+    auto load_w = [&](uint64_t hh, uint32_t& w0, uint32_t& w1) {
+        w0 = w1 = 0u;
+        if (hh < args.H) {
+            w0 = args.W1[hh * kWAnchor + t];
+            if (t + kTcThreads < 193) w1 = args.W1[hh * kWAnchor + t + kTcThreads];
+        }
+    };
+    auto store_w = [&](uint32_t w0, uint32_t w1) {
+        sw[t] = t < 193 ? w0 : 0u;
+        if (t + kTcThreads < 240) sw[t + kTcThreads] = w1;
+    };
+
+    // prologue: W planes of the first anchor, both halves of its MMAs in flight
+    const uint64_t h0 = blockIdx.x;
+    uint32_t nw0, nw1;  // the w words of the NEXT anchor, loaded one iteration early
+    {
+        uint32_t w0, w1;
+        load_w(h0, w0, w1);
+        store_w(w0, w1);
+        load_w(h0 + G, nw0, nw1);
+    }
+    __syncthreads();
+    build_w(0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tmem_base;
+    const uint32_t tmA = tm, tmB = tm + 3 * kTcNA;
+    const uint64_t dA = umma_desc(s0, 2048, 128);
+    const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128);
+    const uint64_t dBbuf = (3 * kTcBPlane) >> 4;  // descriptor step to the other W buffer
+    const uint64_t dBhalf = 1024 >> 4;           // rows m >= 64 start 4 blocks in
+    if (t == 0 && h0 < args.H) {
+        tc_issue_half<kTcNA>(dA, dB0, tmA, barA);
+        tc_issue_half<kTcNB>(dA, dB0 + dBhalf, tmB, barB);
+    }
+    const uint32_t v_base = args.base->v;
+    const uint32_t trow = static_cast<uint32_t>(32 * (t >> 5)) << 16;
+    uint32_t phase = 0;
+    int it = 0;
+    for (uint64_t h = h0; h < args.H; h += G, ++it, phase ^= 1u) {
+        const int buf = it & 1, nbuf = buf ^ 1;
+        const bool has_next = h + G < args.H;
+        // next anchor's w into sw (its W planes are built below) and prefetch the one after
+        store_w(nw0, nw1);
+        load_w(h + 2 * G, nw0, nw1);
+        __syncthreads();
+        if (has_next) build_w(nbuf);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();  // (also: the bulk store that last used staging `buf` has been read)
+        uint8_t* rec = sm + kTcOffOut + buf * kTcOut + 400 * t;
+        const uint64_t row0 = h * kRows;
+        const uint64_t rows = args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows;
+        const bool is_base = args.first == 0 && h == 0 && t == 0;  // stream 0 is the base itself
+        // v of this row's stream, closed form (jump_arith with k J mod m), off the critical path
+        const uint64_t k = args.first + row0 + t;
+        const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
+        const uint32_t v = static_cast<uint32_t>((v_base + (kMod - dec)) % kMod);
+        // ---- half A: m < 64 -> record words 33..96 (+ the tail word group)
+        mbar_wait(&bars[0], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        {
+            uint32_t val[kTcNA];
+            tc_read_half<kTcNA, kTcNA>(tmA + trow, val);
+            if (!is_base) {
+                uint32_t* r32 = reinterpret_cast<uint32_t*>(rec);
+                r32[33] = val[63];
+                r32[34] = val[62];
+                r32[35] = val[61];
+#pragma unroll
+                for (int p = 9; p < 24; ++p)  // words 4p .. 4p + 3 = columns 96 - 4p .. 93 - 4p
+                    reinterpret_cast<uint4*>(rec)[p] =
+                        make_uint4(val[96 - 4 * p], val[95 - 4 * p], val[94 - 4 * p], val[93 - 4 * p]);
+                reinterpret_cast<uint4*>(rec)[24] = make_uint4(val[0], 96u, 32u, v);
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();  // TMEM half A read by everyone; W planes of the next anchor built
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (t == 0 && has_next) tc_issue_half<kTcNA>(dA, dB0 + nbuf * dBbuf, tmA, barA);
+        // ---- half B: 64 <= m < 112 -> record words 0..32
+        mbar_wait(&bars[1], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        {
+            uint32_t val[kTcNB];
+            tc_read_half<kTcNB, kTcNB>(tmB + trow, val);  // val[c] = column 64 + c
+            if (!is_base) {
+#pragma unroll
+                for (int p = 0; p < 8; ++p)  // words 4p .. 4p + 3 = columns 96 - 4p .. 93 - 4p
+                    reinterpret_cast<uint4*>(rec)[p] =
+                        make_uint4(val[32 - 4 * p], val[31 - 4 * p], val[30 - 4 * p], val[29 - 4 * p]);
+                reinterpret_cast<uint32_t*>(rec)[32] = val[0];
+            } else {
+                const uint4* src = reinterpret_cast<const uint4*>(args.base);
+#pragma unroll
+                for (int p = 0; p < 25; ++p) reinterpret_cast<uint4*>(rec)[p] = src[p];
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // records -> bulk copy engine
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (t == 0) {
+            if (has_next) tc_issue_half<kTcNB>(dA, dB0 + nbuf * dBbuf + dBhalf, tmB, barB);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(args.out + row0),
+                         "r"(s0 + kTcOffOut + buf * kTcOut), "r"(static_cast<uint32_t>(rows * 400))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            // staging `nbuf` (the store before this one) must be read before it is rewritten
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -785,13 +1068,14 @@ cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t
 }
 
 namespace {
-std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0};
+std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0};
 }  // namespace
 
 // Shared-memory limits of the jump kernels, raised by ranmar_device_setup so no
 // _dev call (or graph capture) has to do it.
 cudaError_t configure_jump_kernels() {
     if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel, static_cast<int>(kTcSmem), g_cfg_bulk_tc)) return e;
     return ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk);
 }
 
@@ -835,9 +1119,22 @@ cudaError_t launch_copy_state(const ranmar_state* src, ranmar_state* dst, uint32
 cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
                         uint64_t first, uint64_t n, uint32_t jm, const ranmar_state* d_base,
                         int sm_count, cudaStream_t stream) {
+    // tensor-core bulk by default; RANMAR_BULK=imad selects the IMAD kernel (A/B timing)
+    static const bool use_imad = [] {
+        const char* e = std::getenv("RANMAR_BULK");
+        return e && e[0] == 'i';
+    }();
+    const uint64_t grid = H < uint64_t(use_imad ? 2 * sm_count : sm_count) ? H
+                                                                           : uint64_t(use_imad ? 2 * sm_count : sm_count);
+    if (!use_imad) {
+        if (cudaError_t e = ensure_smem(bulk_tc_kernel, static_cast<int>(kTcSmem), g_cfg_bulk_tc)) return e;
+        BulkTcArgs a{W1, H, Tt, out, first, n, jm, d_base};
+        count_launch();
+        bulk_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kTcSmem, stream>>>(a);
+        return cudaGetLastError();
+    }
     if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk)) return e;
     BulkArgs a{W1, H, Tt, out, first, n, jm, d_base};
-    const uint64_t grid = H < uint64_t(2 * sm_count) ? H : uint64_t(2 * sm_count);
     count_launch();
     bulk_kernel<<<static_cast<unsigned>(grid), kBulkThreads, kBulkSmem, stream>>>(a);
     return cudaGetLastError();
