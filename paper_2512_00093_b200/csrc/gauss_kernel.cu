@@ -35,15 +35,35 @@ namespace {
 constexpr int kGT = 64;  // threads (atoms) per block: 24.8 KB of ring, 9 blocks/SM
 constexpr int kBatch = 4;  // accepted pairs per fp64 batch (measured best of 1..8)
 
+// The ring is the kernel's only shared memory, so it starts at the fixed
+// offset of the CTA's shared window where dynamic shared memory begins (after
+// the 1 KB the driver reserves per block on sm_90+). Ring accesses use that
+// offset as the instruction's immediate: LDS/STS [R + 0x400], no base register.
+// Written through a computed base, ptxas re-derives the window base (S2UR
+// SR_CgaCtaId + ULEA) inside the lane-divergent attempt loop, or adds it with an
+// IADD per access. The kernel checks the offset on entry and flags
+// kStatusInternal (no work done) if a driver ever places it elsewhere.
+constexpr uint32_t kRingBase = 0x400;
+
+__device__ __forceinline__ uint32_t ring_ld(uint32_t off) {
+    uint32_t x;
+    asm volatile("ld.shared.u32 %0, [%1+1024];" : "=r"(x) : "r"(off));
+    return x;
+}
+__device__ __forceinline__ void ring_st(uint32_t off, uint32_t x) {
+    asm volatile("st.shared.u32 [%0+1024], %1;" ::"r"(off), "r"(x) : "memory");
+}
+
 template <int K>
 __global__ void __launch_bounds__(kGT)
     gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
                     uint64_t steps, double* __restrict__ out, uint32_t* status) {
-    extern __shared__ uint32_t ring[];  // [97][kGT]
-    // shared-window address of the ring, taken before any divergence so it stays
-    // a uniform register and every ring access is one [R + UR] LDS/STS
-    const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+    extern __shared__ uint32_t ring[];  // [97][kGT], the only shared memory
     const int t = threadIdx.x;
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(ring)) != kRingBase) {
+        if (t == 0) atomicOr(status, kStatusInternal);
+        return;
+    }
     const uint64_t atom = static_cast<uint64_t>(blockIdx.x) * kGT + t;
     if (atom >= n_atoms) return;
     ranmar_gauss_state* gs = g + atom;
@@ -103,11 +123,8 @@ __global__ void __launch_bounds__(kGT)
         uint32_t u[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            uint32_t xa, xb;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(xa) : "r"(rbase + ai));
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(xb) : "r"(rbase + aj));
-            const uint32_t x = xa - xb;
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rbase + ai), "r"(x) : "memory");
+            const uint32_t x = ring_ld(ai) - ring_ld(aj);
+            ring_st(ai, x);
             ai = min(ai - kSlot, top);
             aj = min(aj - kSlot, top);
             v = add_mod_m(v, kStepA);
