@@ -5,8 +5,9 @@
 // PAPER.md:298-324). All coefficient arithmetic is 32-bit mad.lo with
 // wraparound and one final mask: only the low 24 bits of each product matter,
 // which replaces the reference's 64-bit accumulation (polyring.hpp:88-96)
-// without changing a single residue. Tensor cores are not used: this is
-// modular integer arithmetic, not a float contraction.
+// without changing a single residue. Level 0 of make_streams, the one large
+// integer contraction, runs EXACTLY on the tensor cores (bulk_tc_kernel: u8
+// limbs on tcgen05.mma kind::i8, s32 accumulators that cannot overflow).
 //
 //  pow_kernel        K3a  the squaring chain t^(2^k) mod phi in shared memory
 //                         (one CTA, 256 threads split the 9,409 MACs of each
@@ -26,8 +27,11 @@
 //                         2 x 8 register tiles per lane.
 //  level_kernel      K3b  one level of the base-128 stream-start tree
 //                         S_L[k] = apply(S_{L+1}[k / 128], Tab_L[k % 128]).
-//  bulk_kernel       K3b  level 0 (all stream starts): per anchor a 128 x 97
-//                         x 97 integer "GEMM" tile on the IMAD pipe, T^T
+//  bulk_tc_kernel    K3b  level 0 (all stream starts) on the tensor cores
+//                         (see its header below); the default.
+//  bulk_kernel       K3b  the same on the IMAD pipe (RANMAR_BULK=imad, for
+//                         A/B timing): per anchor a 128 x 97
+//                         x 97 integer "GEMM" tile, T^T
 //                         resident in shared memory, double-buffered anchor
 //                         extensions, 4 x 8 register tiles, results stored
 //                         from registers as 16-B vectors.

@@ -66,6 +66,9 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, rows = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    if "Metric Name" in h:  # launch lists may carry DRAM byte counts too: time only
+        mi = h.index("Metric Name")
+        rows = [r for r in rows if len(r) > mi and r[mi] == "gpu__time_duration.sum"]
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     agg = collections.defaultdict(list)
     for r in rows:
