@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
 // next anchor are built (and its w prefetched from HBM two anchors ahead)
 // before that. The CTA's 128 consecutive records (51 KB) leave as ONE TMA
 // bulk store (cp.async.bulk) from a double-buffered staging area.
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;
 constexpr int kTcNA = 64, kTcNB = 48;             // column halves (m < 64, 64 <= m < 112)
 constexpr uint32_t kTcAPlane = 16384;             // 8 K-chunks x 16 row groups x 128 B
 constexpr uint32_t kTcBPlane = 3584;              // 14 blocks x 16 shifts x 16 B
@@ -860,6 +860,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bars[2];  // half A, half B MMA completion
     const int t = threadIdx.x;
+    const int wq = (t >> 5) & 3;   // TMEM lane quarter of this warp: rows 32 wq .. 32 wq + 31
+    const int grp = t >> 7;        // 0: column half A (m < 64), 1: half B (64 <= m < 112)
+    const int row = 32 * wq + (t & 31);
     const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     uint32_t* sw = reinterpret_cast<uint32_t*>(sm + kTcOffW);
     const uint64_t G = gridDim.x;
@@ -894,43 +897,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
-    // W planes of anchor hh into buffer `buf` from sw: chunk (b, s) of plane a =
-    // limb_a(w[16 b + s .. 16 b + s + 15])
+    // W planes of an anchor into buffer `buf` from sw: chunk (b, s) of plane a =
+    // limb_a(w[16 b + s .. 16 b + s + 15]); 224 chunks, one per thread
     auto build_w = [&](int buf) {
-        for (int x = t; x < 14 * 16; x += kTcThreads) {
-            const int o = 16 * (x >> 4) + (x & 15);
+        if (t < 14 * 16) {
+            const int o = 16 * (t >> 4) + (t & 15);
             uint32_t v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = sw[o + e];
 #pragma unroll
             for (uint32_t a = 0; a < 3; ++a)
-                *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * x) =
+                *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * t) =
                     make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
                                limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
         }
     };
-    // this thread's two words of an anchor's extension (zero past 193)
-    auto load_w = [&](uint64_t hh, uint32_t& w0, uint32_t& w1) {
-        w0 = w1 = 0u;
-        if (hh < args.H) {
-            w0 = args.W1[hh * kWAnchor + t];
-            if (t + kTcThreads < 193) w1 = args.W1[hh * kWAnchor + t + kTcThreads];
-        }
+    // this thread's word of an anchor's extension (zero past 193)
+    auto load_w = [&](uint64_t hh) -> uint32_t {
+        return hh < args.H && t < 193 ? args.W1[hh * kWAnchor + t] : 0u;
     };
-    auto store_w = [&](uint32_t w0, uint32_t w1) {
-        sw[t] = t < 193 ? w0 : 0u;
-        if (t + kTcThreads < 240) sw[t + kTcThreads] = w1;
+    auto store_w = [&](uint32_t w0) {
+        if (t < 240) sw[t] = w0;
     };
 
     // prologue: W planes of the first anchor, both halves of its MMAs in flight
     const uint64_t h0 = blockIdx.x;
-    uint32_t nw0, nw1;  // the w words of the NEXT anchor, loaded one iteration early
-    {
-        uint32_t w0, w1;
-        load_w(h0, w0, w1);
-        store_w(w0, w1);
-        load_w(h0 + G, nw0, nw1);
-    }
+    uint32_t nw = load_w(h0 + G);  // the w word of the NEXT anchor, loaded one iteration early
+    store_w(load_w(h0));
     __syncthreads();
     build_w(0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -948,31 +941,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         tc_issue_half<kTcNB>(dA, dB0 + dBhalf, tmB, barB);
     }
     const uint32_t v_base = args.base->v;
-    const uint32_t trow = static_cast<uint32_t>(32 * (t >> 5)) << 16;
+    const uint32_t trow = static_cast<uint32_t>(32 * wq) << 16;
     uint32_t phase = 0;
     int it = 0;
+    // Per anchor h: the W planes of h + 1 are built while the tensor core computes
+    // both halves of h; then the two 4-warp groups read the halves back from TMEM
+    // concurrently (group 0 columns 0..63, group 1 columns 64..111, each warp its
+    // lane quarter = 32 rows), combine the limbs and write their part of each
+    // record; one barrier later the MMAs of h + 1 and the bulk store of h go out.
     for (uint64_t h = h0; h < args.H; h += G, ++it, phase ^= 1u) {
         const int buf = it & 1, nbuf = buf ^ 1;
         const bool has_next = h + G < args.H;
-        // next anchor's w into sw (its W planes are built below) and prefetch the one after
-        store_w(nw0, nw1);
-        load_w(h + 2 * G, nw0, nw1);
-        __syncthreads();
+        store_w(nw);
+        nw = load_w(h + 2 * G);
+        __syncthreads();  // (also: the bulk store that last used staging `buf` has been read)
         if (has_next) build_w(nbuf);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();  // (also: the bulk store that last used staging `buf` has been read)
-        uint8_t* rec = sm + kTcOffOut + buf * kTcOut + 400 * t;
+        uint8_t* rec = sm + kTcOffOut + buf * kTcOut + 400 * row;
         const uint64_t row0 = h * kRows;
         const uint64_t rows = args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows;
-        const bool is_base = args.first == 0 && h == 0 && t == 0;  // stream 0 is the base itself
-        // v of this row's stream, closed form (jump_arith with k J mod m), off the critical path
-        const uint64_t k = args.first + row0 + t;
-        const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
-        const uint32_t v = static_cast<uint32_t>((v_base + (kMod - dec)) % kMod);
-        // ---- half A: m < 64 -> record words 33..96 (+ the tail word group)
-        mbar_wait(&bars[0], phase);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        {
+        const bool is_base = args.first == 0 && h == 0 && row == 0;  // stream 0 is the base itself
+        if (grp == 0) {
+            // v of this row's stream, closed form (jump_arith with k J mod m)
+            const uint64_t k = args.first + row0 + row;
+            const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
+            const uint32_t v = static_cast<uint32_t>((v_base + (kMod - dec)) % kMod);
+            // ---- half A: m < 64 -> record words 33..96 (+ the tail word group)
+            mbar_wait(&bars[0], phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             uint32_t val[kTcNA];
             tc_read_half<kTcNA, kTcNA>(tmA + trow, val);
             if (!is_base) {
@@ -986,15 +982,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
                         make_uint4(val[96 - 4 * p], val[95 - 4 * p], val[94 - 4 * p], val[93 - 4 * p]);
                 reinterpret_cast<uint4*>(rec)[24] = make_uint4(val[0], 96u, 32u, v);
             }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // TMEM half A read by everyone; W planes of the next anchor built
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (t == 0 && has_next) tc_issue_half<kTcNA>(dA, dB0 + nbuf * dBbuf, tmA, barA);
-        // ---- half B: 64 <= m < 112 -> record words 0..32
-        mbar_wait(&bars[1], phase);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        {
+        } else {
+            // ---- half B: 64 <= m < 112 -> record words 0..32
+            mbar_wait(&bars[1], phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             uint32_t val[kTcNB];
             tc_read_half<kTcNB, kTcNB>(tmB + trow, val);  // val[c] = column 64 + c
             if (!is_base) {
@@ -1011,10 +1002,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // records -> bulk copy engine
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
+        __syncthreads();  // TMEM read by everyone, W planes of h + 1 built, records complete
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (t == 0) {
-            if (has_next) tc_issue_half<kTcNB>(dA, dB0 + nbuf * dBbuf + dBhalf, tmB, barB);
+            if (has_next) {
+                tc_issue_half<kTcNA>(dA, dB0 + nbuf * dBbuf, tmA, barA);
+                tc_issue_half<kTcNB>(dA, dB0 + nbuf * dBbuf + dBhalf, tmB, barB);
+            }
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(args.out + row0),
                          "r"(s0 + kTcOffOut + buf * kTcOut), "r"(static_cast<uint32_t>(rows * 400))
                          : "memory");

@@ -584,12 +584,22 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     uint32_t* V1 = reinterpret_cast<uint32_t*>(ws + p.off_v1);
 
     // K3a: Q_b = P_{2^b J} = prod_{k in bits(J)} Z_{k+b} for b < 7 * levels and,
-    // if first > 0, P_{first J}; all independent, one launch.
+    // if first > 0, P_{first J}; all independent, one launch. When J = 2^k (the
+    // usual block length, configs 2-5) Q_b = Z_{k+b} are consecutive rows of the
+    // square table and are read in place: no launch.
+    int jbit = -1, jpop = 0;
+    for (int k = 0; k < 256; ++k)
+        if ((J.w[k >> 6] >> (k & 63)) & 1u) {
+            jbit = k;
+            ++jpop;
+        }
+    const bool q_in_table = jpop == 1 && jbit + 7 * p.tab_levels <= kSquares;
+    const uint32_t* Qsrc = q_in_table ? Z + size_t(jbit) * kPolyN : Q;
     uint64_t e[kMaxPlanPows][4];
     int shift[kMaxPlanPows];
     uint32_t* outs[kMaxPlanPows];
     int njobs = 0;
-    for (int b = 0; b < 7 * p.tab_levels; ++b, ++njobs) {
+    for (int b = 0; !q_in_table && b < 7 * p.tab_levels; ++b, ++njobs) {
         std::memcpy(e[njobs], J.w, sizeof J.w);
         shift[njobs] = b;
         outs[njobs] = Q + size_t(b) * kPolyN;
@@ -600,9 +610,9 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
         outs[njobs] = Pf;
         ++njobs;
     }
-    RB_CUDA(rb::launch_pow_table(e, shift, outs, njobs, Z, s), "pow_table_kernel launch");
+    if (njobs) RB_CUDA(rb::launch_pow_table(e, shift, outs, njobs, Z, s), "pow_table_kernel launch");
     // Offset tables Tab_L[r] = P_{r 128^L J}.
-    RB_CUDA(rb::launch_tables(Q, p.tab_levels, Tab, Tt, s), "tables_kernel launch");
+    RB_CUDA(rb::launch_tables(Qsrc, p.tab_levels, Tab, Tt, s), "tables_kernel launch");
     // The base state, in the workspace; A_0 = s_{first J}.
     if (h_base) {
         RB_CUDA(rb::launch_put_state(*h_base, dbase, s), "put_state launch");
