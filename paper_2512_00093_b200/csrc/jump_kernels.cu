@@ -773,15 +773,18 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
 // next anchor are built (and its w prefetched from HBM two anchors ahead)
 // before that. The CTA's 128 consecutive records (51 KB) leave as ONE TMA
 // bulk store (cp.async.bulk) from a double-buffered staging area.
-constexpr int kTcThreads = 256;
+constexpr int kTcConsumerWarps = 8;
+constexpr int kTcThreads = 32 * (kTcConsumerWarps + 1);  // + the MMA / bulk-store producer warp
 constexpr int kTcNA = 64, kTcNB = 48;             // column halves (m < 64, 64 <= m < 112)
 constexpr uint32_t kTcAPlane = 16384;             // 8 K-chunks x 16 row groups x 128 B
 constexpr uint32_t kTcBPlane = 3584;              // 14 blocks x 16 shifts x 16 B
-constexpr uint32_t kTcOffB = 3 * kTcAPlane;                 // 2 buffers x 3 planes
+constexpr uint32_t kTcOffB = 0;                             // 2 buffers x 3 planes
 constexpr uint32_t kTcOffW = kTcOffB + 2 * 3 * kTcBPlane;   // 240 words of w
-constexpr uint32_t kTcOffOut = kTcOffW + 1024;              // 2 x 128 records x 400 B
+constexpr uint32_t kTcOffOut = kTcOffW + 1024;              // kTcStages x 128 records x 400 B
+constexpr int kTcStages = 3;  // record staging buffers: up to 3 bulk stores in flight per SM
 constexpr uint32_t kTcOut = 128 * 400;
-constexpr uint32_t kTcSmem = kTcOffOut + 2 * kTcOut;        // 172 KB: one CTA per SM
+constexpr uint32_t kTcSmem = kTcOffOut + kTcStages * kTcOut;  // 173 KB: one CTA per SM
+constexpr uint32_t kTcColT = 3 * 64 + 3 * 48;               // TMEM columns of the T limbs (96)
 static_assert(kTcSmem <= 227 * 1024, "tensor-core bulk smem");
 
 struct BulkTcArgs {
@@ -807,25 +810,28 @@ __device__ __forceinline__ uint32_t limb4(uint32_t w0, uint32_t w1, uint32_t w2,
 
 // The 24 MMAs of one column half: D0 += T0 W0; D1 += T0 W1 + T1 W0;
 // D2 += T0 W2 + T1 W1 + T2 W0 (K = 128 in 4 steps), then a commit to `bar`.
-// dA / dB: descriptors of limb plane 0 at K-step 0; planes and K steps are
-// offsets added to the 14-bit start-address field (addresses < 256 KB, no carry).
+// The T limbs (operand A) live in TMEM: limb a, K-step ks at columns tmT +
+// (4 a + ks) 8 (32 i8 per row = 8 columns); only the per-anchor W planes
+// (operand B, descriptor dB = limb plane 0 at K-step 0) are read from shared
+// memory. With A in shared memory too, the tensor core's operand reads (276 KB
+// per anchor) saturated the SM's shared-memory bandwidth.
 template <int N>
-__device__ __forceinline__ void tc_issue_half(uint64_t dA, uint64_t dB, uint32_t tmem, uint32_t bar) {
+__device__ __forceinline__ void tc_issue_half(uint32_t tmT, uint64_t dB, uint32_t tmem, uint32_t bar) {
     constexpr uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (8u << 24);
     constexpr uint32_t ta[6] = {0, 0, 1, 0, 1, 2}, tb[6] = {0, 1, 0, 2, 1, 0}, td[6] = {0, 1, 1, 2, 2, 2};
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t da = dA + ((ta[p] * kTcAPlane + ks * 4096) >> 4);
+            const uint32_t ta_addr = tmT + (ta[p] * 4 + ks) * 8;
             const uint64_t db = dB + ((tb[p] * kTcBPlane + ks * 512) >> 4);
             if ((p == 0 || p == 1 || p == 3) && ks == 0) {  // first product of an accumulator
-                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;" ::"r"(tmem + td[p] * N),
-                             "l"(da), "l"(db), "r"(idesc)
+                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 0;" ::"r"(tmem + td[p] * N),
+                             "r"(ta_addr), "l"(db), "r"(idesc)
                              : "memory");
             } else {
-                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(tmem + td[p] * N),
-                             "l"(da), "l"(db), "r"(idesc)
+                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;" ::"r"(tmem + td[p] * N),
+                             "r"(ta_addr), "l"(db), "r"(idesc)
                              : "memory");
             }
         }
@@ -834,193 +840,268 @@ __device__ __forceinline__ void tc_issue_half(uint64_t dA, uint64_t dB, uint32_t
                  : "memory");
 }
 
-// Columns [c0, c0 + NC) of this thread's row: (D0 + 2^8 D1 + 2^16 D2) & mask.
-template <int NC, int N>
-__device__ __forceinline__ void tc_read_half(uint32_t trow, uint32_t (&val)[NC]) {
+// 16 columns of this thread's TMEM row starting at column `col` of an
+// accumulator set with N columns per accumulator: (D0 + 2^8 D1 + 2^16 D2) & mask.
+template <int N>
+__device__ __forceinline__ void tc_read_chunk(uint32_t taddr, uint32_t (&val)[16]) {
+    uint32_t d[3][16];
 #pragma unroll
-    for (int c0 = 0; c0 < NC; c0 += 16) {
-        uint32_t d[3][16];
+    for (int a = 0; a < 3; ++a)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(d[a][0]), "=r"(d[a][1]), "=r"(d[a][2]), "=r"(d[a][3]), "=r"(d[a][4]), "=r"(d[a][5]),
+              "=r"(d[a][6]), "=r"(d[a][7]), "=r"(d[a][8]), "=r"(d[a][9]), "=r"(d[a][10]), "=r"(d[a][11]),
+              "=r"(d[a][12]), "=r"(d[a][13]), "=r"(d[a][14]), "=r"(d[a][15])
+            : "r"(taddr + a * N));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(d[a][0]), "=r"(d[a][1]), "=r"(d[a][2]), "=r"(d[a][3]), "=r"(d[a][4]), "=r"(d[a][5]),
-                  "=r"(d[a][6]), "=r"(d[a][7]), "=r"(d[a][8]), "=r"(d[a][9]), "=r"(d[a][10]), "=r"(d[a][11]),
-                  "=r"(d[a][12]), "=r"(d[a][13]), "=r"(d[a][14]), "=r"(d[a][15])
-                : "r"(trow + a * N + c0));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < 16; ++q) val[c0 + q] = (d[0][q] + (d[1][q] << 8) + (d[2][q] << 16)) & kMask;
-    }
+    for (int q = 0; q < 16; ++q) val[q] = (d[0][q] + (d[1][q] << 8) + (d[2][q] << 16)) & kMask;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_constant__ BulkTcArgs args) {
     extern __shared__ __align__(1024) uint32_t tc_smem[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(tc_smem);
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) uint64_t bars[2];  // half A, half B MMA completion
+    // mbarriers: MMA half A / B complete (tcgen05.commit), TMEM half A / B drained
+    // (8 consumer warps), W planes of buffer b built (8), records of staging b
+    // written (8), staging b read by its bulk store (the producer)
+    __shared__ __align__(8) uint64_t bars[6];
+    enum { kMmaA = 0, kMmaB = 1, kFreeA = 2, kFreeB = 3, kWReady = 4 };
     const int t = threadIdx.x;
-    const int wq = (t >> 5) & 3;   // TMEM lane quarter of this warp: rows 32 wq .. 32 wq + 31
-    const int grp = t >> 7;        // 0: column half A (m < 64), 1: half B (64 <= m < 112)
-    const int row = 32 * wq + (t & 31);
+    const int warp = t >> 5, lane = t & 31;
     const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+    auto bar = [&](int k) { return b0 + 8u * static_cast<uint32_t>(k); };
     uint32_t* sw = reinterpret_cast<uint32_t*>(sm + kTcOffW);
     const uint64_t G = gridDim.x;
 
-    // A planes (T limbs), once per CTA: row r, K-chunk c -> (c * 16 + r / 8) * 128 + (r % 8) * 16
-    for (int x = t; x < 128 * 8; x += kTcThreads) {
-        const int r = x & 127, c = x >> 7;  // consecutive threads: consecutive rows (coalesced Tt reads)
-        uint32_t v[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int k = 16 * c + e;
-            v[e] = k < kPolyN ? args.Tt[k * kRows + r] : 0u;
-        }
-        const uint32_t off = static_cast<uint32_t>((c * 16 + (r >> 3)) * 128 + (r & 7) * 16);
-#pragma unroll
-        for (uint32_t a = 0; a < 3; ++a)
-            *reinterpret_cast<uint4*>(sm + a * kTcAPlane + off) =
-                make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
-                           limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
-    }
-    if (t < 32) {
+    if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                          static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    const uint32_t barA = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]));
-    const uint32_t barB = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]));
     if (t == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barA) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barB) : "memory");
+        const uint32_t cnt[6] = {1, 1, 8, 8, 8, 8};
+        for (int k = 0; k < 6; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar(k)), "r"(cnt[k]) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-
-    // W planes of an anchor into buffer `buf` from sw: chunk (b, s) of plane a =
-    // limb_a(w[16 b + s .. 16 b + s + 15]); 224 chunks, one per thread
-    auto build_w = [&](int buf) {
-        if (t < 14 * 16) {
-            const int o = 16 * (t >> 4) + (t & 15);
-            uint32_t v[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = sw[o + e];
-#pragma unroll
-            for (uint32_t a = 0; a < 3; ++a)
-                *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * t) =
-                    make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
-                               limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
-        }
-    };
-    // this thread's word of an anchor's extension (zero past 193)
-    auto load_w = [&](uint64_t hh) -> uint32_t {
-        return hh < args.H && t < 193 ? args.W1[hh * kWAnchor + t] : 0u;
-    };
-    auto store_w = [&](uint32_t w0) {
-        if (t < 240) sw[t] = w0;
-    };
-
-    // prologue: W planes of the first anchor, both halves of its MMAs in flight
-    const uint64_t h0 = blockIdx.x;
-    uint32_t nw = load_w(h0 + G);  // the w word of the NEXT anchor, loaded one iteration early
-    store_w(load_w(h0));
-    __syncthreads();
-    build_w(0);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm = tmem_base;
-    const uint32_t tmA = tm, tmB = tm + 3 * kTcNA;
-    const uint64_t dA = umma_desc(s0, 2048, 128);
-    const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128);
-    const uint64_t dBbuf = (3 * kTcBPlane) >> 4;  // descriptor step to the other W buffer
-    const uint64_t dBhalf = 1024 >> 4;           // rows m >= 64 start 4 blocks in
-    if (t == 0 && h0 < args.H) {
-        tc_issue_half<kTcNA>(dA, dB0, tmA, barA);
-        tc_issue_half<kTcNB>(dA, dB0 + dBhalf, tmB, barB);
-    }
-    const uint32_t v_base = args.base->v;
-    const uint32_t trow = static_cast<uint32_t>(32 * wq) << 16;
-    uint32_t phase = 0;
-    int it = 0;
-    // Per anchor h: the W planes of h + 1 are built while the tensor core computes
-    // both halves of h; then the two 4-warp groups read the halves back from TMEM
-    // concurrently (group 0 columns 0..63, group 1 columns 64..111, each warp its
-    // lane quarter = 32 rows), combine the limbs and write their part of each
-    // record; one barrier later the MMAs of h + 1 and the bulk store of h go out.
-    for (uint64_t h = h0; h < args.H; h += G, ++it, phase ^= 1u) {
-        const int buf = it & 1, nbuf = buf ^ 1;
-        const bool has_next = h + G < args.H;
-        store_w(nw);
-        nw = load_w(h + 2 * G);
-        __syncthreads();  // (also: the bulk store that last used staging `buf` has been read)
-        if (has_next) build_w(nbuf);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        uint8_t* rec = sm + kTcOffOut + buf * kTcOut + 400 * row;
-        const uint64_t row0 = h * kRows;
-        const uint64_t rows = args.n - row0 < (uint64_t)kRows ? args.n - row0 : (uint64_t)kRows;
-        const bool is_base = args.first == 0 && h == 0 && row == 0;  // stream 0 is the base itself
-        if (grp == 0) {
-            // v of this row's stream, closed form (jump_arith with k J mod m)
-            const uint64_t k = args.first + row0 + row;
-            const uint64_t dec = ((k % kMod) * args.jm % kMod) * kDelta % kMod;
-            const uint32_t v = static_cast<uint32_t>((v_base + (kMod - dec)) % kMod);
-            // ---- half A: m < 64 -> record words 33..96 (+ the tail word group)
-            mbar_wait(&bars[0], phase);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t val[kTcNA];
-            tc_read_half<kTcNA, kTcNA>(tmA + trow, val);
-            if (!is_base) {
-                uint32_t* r32 = reinterpret_cast<uint32_t*>(rec);
-                r32[33] = val[63];
-                r32[34] = val[62];
-                r32[35] = val[61];
+    const uint32_t tmA = tm, tmB = tm + 3 * kTcNA, tmT = tm + kTcColT;
+    // T limbs into TMEM once per CTA (warps 0-3, one row each): row r, limb a, K-step
+    // ks, column c holds limb a of T[r][32 ks + 4 c .. + 3] (coalesced Tt reads)
+    if (warp < 4) {
+        const int r = t;
 #pragma unroll
-                for (int p = 9; p < 24; ++p)  // words 4p .. 4p + 3 = columns 96 - 4p .. 93 - 4p
-                    reinterpret_cast<uint4*>(rec)[p] =
-                        make_uint4(val[96 - 4 * p], val[95 - 4 * p], val[94 - 4 * p], val[93 - 4 * p]);
-                reinterpret_cast<uint4*>(rec)[24] = make_uint4(val[0], 96u, 32u, v);
+        for (int ks = 0; ks < 4; ++ks) {
+            uint32_t v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const int k = 32 * ks + e;
+                v[e] = k < kPolyN ? args.Tt[k * kRows + r] : 0u;
             }
-        } else {
-            // ---- half B: 64 <= m < 112 -> record words 0..32
-            mbar_wait(&bars[1], phase);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t val[kTcNB];
-            tc_read_half<kTcNB, kTcNB>(tmB + trow, val);  // val[c] = column 64 + c
-            if (!is_base) {
 #pragma unroll
-                for (int p = 0; p < 8; ++p)  // words 4p .. 4p + 3 = columns 96 - 4p .. 93 - 4p
-                    reinterpret_cast<uint4*>(rec)[p] =
-                        make_uint4(val[32 - 4 * p], val[31 - 4 * p], val[30 - 4 * p], val[29 - 4 * p]);
-                reinterpret_cast<uint32_t*>(rec)[32] = val[0];
-            } else {
+            for (uint32_t a = 0; a < 3; ++a) {
+                uint32_t q[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) q[c] = limb4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], a);
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                        tmT + (static_cast<uint32_t>(32 * warp) << 16) + (a * 4 + ks) * 8),
+                    "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]), "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(q[7])
+                    : "memory");
+            }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint64_t h0 = blockIdx.x;
+    const uint32_t n_anchor = h0 < args.H ? static_cast<uint32_t>((args.H - 1 - h0) / G + 1) : 0u;
+
+    if (warp == kTcConsumerWarps) {
+        // ---------------- producer: one thread issues the MMAs
+        if (lane == 0 && n_anchor) {
+            const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128);
+            const uint64_t dBbuf = (3 * kTcBPlane) >> 4;  // descriptor step to the other W buffer
+            const uint64_t dBhalf = 1024 >> 4;           // rows m' >= 64 start 4 blocks in
+            mbar_wait_a(bar(kWReady), 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tc_issue_half<kTcNA>(tmT, dB0, tmA, bar(kMmaA));
+            tc_issue_half<kTcNB>(tmT, dB0 + dBhalf, tmB, bar(kMmaB));
+            for (uint32_t i = 0; i < n_anchor; ++i) {
+                const uint32_t nb = (i + 1) & 1;
+                if (i + 1 < n_anchor) {
+                    mbar_wait_a(bar(kWReady + nb), ((i + 1) >> 1) & 1);
+                    mbar_wait_a(bar(kFreeA), i & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    tc_issue_half<kTcNA>(tmT, dB0 + nb * dBbuf, tmA, bar(kMmaA));
+                    mbar_wait_a(bar(kFreeB), i & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    tc_issue_half<kTcNB>(tmT, dB0 + nb * dBbuf + dBhalf, tmB, bar(kMmaB));
+                }
+            }
+        }
+    } else if (n_anchor) {
+        // ---------------- 8 consumer warps: W planes, TMEM read-back, records
+        const int wq = warp & 3;       // TMEM lane quarter: rows 32 wq .. 32 wq + 31
+        const int sub = warp >> 2;     // which of the two warps of this quarter
+        const int row = 32 * wq + lane;
+        const uint32_t trow = static_cast<uint32_t>(32 * wq) << 16;
+        const uint32_t v_base = args.base->v;
+        // w shifted by 3 (sw[n] = w[n - 3]): output column m' = m + 3 is state word
+        // 99 - m', so every 16-column chunk maps onto four whole 16-B record groups
+        auto load_w = [&](uint64_t hh) -> uint32_t {
+            return hh < args.H && t >= 3 && t < 196 ? args.W1[hh * kWAnchor + t - 3] : 0u;
+        };
+        auto store_w = [&](uint32_t w0) {
+            if (t < 240) sw[t] = w0;
+        };
+        auto cbar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        // the two warps of a lane quarter
+        auto qbar = [&] { asm volatile("bar.sync %0, 64;" ::"r"(2 + wq) : "memory"); };
+        // W planes into buffer `buf` from sw: chunk (b, s) of plane a = limb_a(sw[16 b + s ..
+        // 16 b + s + 15]); 224 chunks over the 256 consumer threads
+        auto build_w = [&](int buf) {
+            if (t < 14 * 16) {
+                const int o = 16 * (t >> 4) + (t & 15);
+                uint32_t v[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = sw[o + e];
+#pragma unroll
+                for (uint32_t a = 0; a < 3; ++a)
+                    *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * t) =
+                        make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
+                                   limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(kWReady + buf));
+        };
+        // chunk c (columns m' = 16 c .. 16 c + 15) of this row -> record groups 24 - 4 c - q
+        auto put_chunk = [&](uint8_t* rec, int c, const uint32_t (&val)[16], uint32_t v) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int g = 24 - 4 * c - q;
+                if (g < 0) break;
+                uint4 x = make_uint4(val[4 * q + 3], val[4 * q + 2], val[4 * q + 1], val[4 * q]);
+                if (g == 24) x = make_uint4(val[3], 96u, 32u, v);  // word 96, then i, j, v
+                reinterpret_cast<uint4*>(rec)[g] = x;
+            }
+        };
+        // v of this row's stream k (jump_arith: v_base - k (J mod m) d mod m), then
+        // stepped by the 128 G streams between this thread's consecutive anchors
+        const uint64_t dstep = static_cast<uint64_t>(args.jm) * kDelta % kMod;  // per stream
+        uint32_t vrow, vstep;
+        {
+            const uint64_t k = args.first + h0 * kRows + row;
+            vrow = static_cast<uint32_t>((v_base + kMod - (k % kMod) * dstep % kMod) % kMod);
+            vstep = static_cast<uint32_t>((kRows * G) % kMod * dstep % kMod);
+        }
+        store_w(load_w(h0));
+        uint32_t nw = load_w(h0 + G);
+        cbar();
+        build_w(0);
+        for (uint32_t i = 0; i < n_anchor; ++i) {
+            const uint64_t h = h0 + i * G;
+            const uint32_t sb = i % kTcStages;
+            cbar();  // everyone's build_w has read sw
+            if (i + 1 < n_anchor) {
+                store_w(nw);
+                cbar();
+                build_w((i + 1) & 1);  // its previous MMAs (anchor i - 1) completed in iteration i - 1
+            }
+            nw = load_w(h + 2 * G);
+            // this quarter's staging of anchor i - kTcStages has been read by its bulk store
+            if (sub == 0 && lane == 0 && i >= kTcStages)
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTcStages - 1) : "memory");
+            qbar();
+            uint8_t* rec = sm + kTcOffOut + sb * kTcOut + 400 * row;
+            const uint64_t row0 = h * kRows;
+            const bool is_base = args.first == 0 && h == 0 && row == 0;  // stream 0 is the base itself
+            const uint32_t v = vrow;
+            vrow = vrow >= vstep ? vrow - vstep : vrow + (kMod - vstep);  // stream k + 128 G
+            // half A: chunks 0..3, two per warp of the quarter
+            mbar_wait_a(bar(kMmaA), i & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = 2 * sub + cc;
+                uint32_t val[16];
+                tc_read_chunk<kTcNA>(tmA + trow + 16 * c, val);
+                if (!is_base) put_chunk(rec, c, val, v);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(kFreeA));
+            // half B: chunks 4..6 (sub 0: 4 and 5, sub 1: 6)
+            mbar_wait_a(bar(kMmaB), i & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (sub == 0) {
+#pragma unroll
+                for (int c = 4; c < 6; ++c) {
+                    uint32_t val[16];
+                    tc_read_chunk<kTcNB>(tmB + trow + 16 * (c - 4), val);
+                    if (!is_base) put_chunk(rec, c, val, v);
+                }
+            } else {  // chunk 6: only m' = 96..99 (state words 3..0) are state words
+                uint32_t d[3][4];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(d[a][0]), "=r"(d[a][1]), "=r"(d[a][2]), "=r"(d[a][3])
+                                 : "r"(tmB + trow + 32 + a * kTcNB));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                uint32_t val[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) val[q] = (d[0][q] + (d[1][q] << 8) + (d[2][q] << 16)) & kMask;
+                if (!is_base) reinterpret_cast<uint4*>(rec)[0] = make_uint4(val[3], val[2], val[1], val[0]);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            if (is_base && warp == 0) {
                 const uint4* src = reinterpret_cast<const uint4*>(args.base);
 #pragma unroll
                 for (int p = 0; p < 25; ++p) reinterpret_cast<uint4*>(rec)[p] = src[p];
             }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // records -> bulk copy engine
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // TMEM read by everyone, W planes of h + 1 built, records complete
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (t == 0) {
-            if (has_next) {
-                tc_issue_half<kTcNA>(dA, dB0 + nbuf * dBbuf, tmA, barA);
-                tc_issue_half<kTcNB>(dA, dB0 + nbuf * dBbuf + dBhalf, tmB, barB);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // records -> bulk copy engine
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(kFreeB));
+            // the quarter's 32 consecutive records (12.8 KB) leave as one bulk store,
+            // issued by its first warp: four stores per anchor, up to kTcStages in flight
+            qbar();
+            if (sub == 0 && lane == 0) {
+                const uint64_t r0 = row0 + 32 * wq;
+                const uint64_t nr = args.n > r0 ? (args.n - r0 < 32 ? args.n - r0 : 32) : 0;
+                if (nr)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(args.out + r0),
+                                 "r"(s0 + kTcOffOut + sb * kTcOut + 400u * 32u * wq), "r"(static_cast<uint32_t>(nr * 400))
+                                 : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(args.out + row0),
-                         "r"(s0 + kTcOffOut + buf * kTcOut), "r"(static_cast<uint32_t>(rows * 400))
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            // staging `nbuf` (the store before this one) must be read before it is rewritten
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
+        if (sub == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
 }  // namespace
