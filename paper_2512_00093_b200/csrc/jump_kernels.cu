@@ -802,6 +802,17 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
            (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (static_cast<uint64_t>(1) << 46);
 }
 
+// The three u8 limbs of four coefficients at once (7 PRMTs instead of 9):
+// l_a = byte a of w0..w3 packed little-endian.
+__device__ __forceinline__ void limbs3(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t& l0,
+                                       uint32_t& l1, uint32_t& l2) {
+    const uint32_t x = __byte_perm(w0, w1, 0x5140);  // w0.b0 w1.b0 w0.b1 w1.b1
+    const uint32_t y = __byte_perm(w2, w3, 0x5140);  // w2.b0 w3.b0 w2.b1 w3.b1
+    l0 = __byte_perm(x, y, 0x5410);
+    l1 = __byte_perm(x, y, 0x7632);
+    l2 = __byte_perm(__byte_perm(w0, w1, 0x0062), __byte_perm(w2, w3, 0x6200), 0x7610);
+}
+
 // byte a of each of w0..w3 packed little-endian (the limb a of four coefficients)
 __device__ __forceinline__ uint32_t limb4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t a) {
     const uint32_t sel = a | ((a + 4) << 4);
@@ -983,14 +994,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         auto build_w = [&](int buf) {
             if (t < 14 * 16) {
                 const int o = 16 * (t >> 4) + (t & 15);
-                uint32_t v[16];
+                uint32_t v[16], q[3][4];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) v[e] = sw[o + e];
 #pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    limbs3(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], q[0][c], q[1][c], q[2][c]);
+#pragma unroll
                 for (uint32_t a = 0; a < 3; ++a)
                     *reinterpret_cast<uint4*>(sm + kTcOffB + (3 * buf + a) * kTcBPlane + 16 * t) =
-                        make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
-                                   limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
+                        make_uint4(q[a][0], q[a][1], q[a][2], q[a][3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -1104,6 +1117,260 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
+// ---- batched jump_state on the TENSOR CORES: out_s = u_s * P(A) for 128
+// states per tile, with one shared P (jump.hpp:60-76). As a GEMM with the
+// states on M: OUT[s][m] = sum_i W_s[i] p[i - m] (W_s = the 193-term recurrence
+// extension of state s's canonical vector, i < 193 -> K padded to 224). The
+// shared operand p[i - m] is Toeplitz in (m, i); with the output columns
+// reversed, m~ = 108 - m, it is Hankel: B[m~][i] = pp[m~ + i], pp[n] =
+// p[n - 108], so the shifted-copy layout of bulk_tc_kernel describes it
+// (leading/stride byte offsets 256/128), built once per CTA. Column m~ is
+// state word m~ - 12, so each 16-column chunk is four whole 16-B record
+// groups. The per-tile operand (the states' extensions, u8 limbs) goes to
+// TMEM (168 columns next to the 336 accumulator columns): A from TMEM, B from
+// shared memory, six u8 x u8 -> s32 GEMMs of 128 x 112 x 224 per tile, exact
+// as in bulk_tc_kernel. One 8-warp CTA per SM; warps w and w + 4 share the
+// tile's states 32 w .. 32 w + 31 (their TMEM lane quarter) and split each phase.
+constexpr int kAtThreads = 256;                       // two warps per TMEM lane quarter
+constexpr int kAtN = 112;
+constexpr int kAtKSteps = 7;                          // K = 224
+constexpr uint32_t kAtBPlane = 21 * 16 * 16;          // (7 + 14) blocks x 16 shifts x 16 B
+constexpr int kAtWStride = 196;                       // 16-B rows: LDS.128 per lane, 4 wavefronts
+constexpr uint32_t kAtOffW = 3 * kAtBPlane;
+constexpr uint32_t kAtOffRaw = kAtOffW + 128 * kAtWStride * 4;  // the next tile's raw records
+constexpr uint32_t kAtSmem = kAtOffRaw + 128 * 400 + 128 * 4;   // + canonical cursors: 168 KB
+constexpr uint32_t kAtColA = 3 * kAtN;                // TMEM: accumulators, then the A limbs
+
+__global__ void __launch_bounds__(kAtThreads, 1)
+    apply_tc_kernel(const ranmar_state* __restrict__ in, ranmar_state* __restrict__ out, uint64_t n,
+                    const uint32_t* __restrict__ P, uint32_t dec, uint32_t* status) {
+    extern __shared__ __align__(1024) uint32_t at_smem[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>(at_smem);
+    uint32_t* W = reinterpret_cast<uint32_t*>(sm + kAtOffW);
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t mma_bar, raw_bar_s;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int wq = warp & 3, sub = warp >> 2;  // TMEM lane quarter, which warp of the quarter
+    const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mma_bar));
+    const uint32_t raw_bar = static_cast<uint32_t>(__cvta_generic_to_shared(&raw_bar_s));
+
+    // B planes from p: item x = 16 b + s holds limbs of pp[16 b + s .. + 15]
+    for (int x = t; x < 21 * 16; x += kAtThreads) {
+        const int o = 16 * (x >> 4) + (x & 15);
+        uint32_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int j = o + e - 108;
+            v[e] = j >= 0 && j < kPolyN ? P[j] : 0u;
+        }
+#pragma unroll
+        for (uint32_t a = 0; a < 3; ++a)
+            *reinterpret_cast<uint4*>(sm + a * kAtBPlane + 16 * x) =
+                make_uint4(limb4(v[0], v[1], v[2], v[3], a), limb4(v[4], v[5], v[6], v[7], a),
+                           limb4(v[8], v[9], v[10], v[11], a), limb4(v[12], v[13], v[14], v[15], a));
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(raw_bar) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B planes -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tmem_base;
+    const uint32_t tmA = tm + kAtColA;
+    const uint32_t tq = static_cast<uint32_t>(32 * wq) << 16;  // this warp's TMEM lane quarter
+    const uint64_t dB = umma_desc(s0, 256, 128);
+    constexpr uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(kAtN >> 3) << 17) | (8u << 24);
+    const uint64_t n_tiles = (n + 127) / 128;
+    uint32_t phase = 0;
+    const uint4* raw4 = reinterpret_cast<const uint4*>(sm + kAtOffRaw);
+    int* ci = reinterpret_cast<int*>(sm + kAtOffRaw + 128 * 400);  // canonical cursor per state
+    if (t == 0 && blockIdx.x < n_tiles) {  // the first tile's raw records
+        const uint64_t sb0 = static_cast<uint64_t>(blockIdx.x) * 128;
+        const uint32_t bytes = static_cast<uint32_t>((n - sb0 < 128 ? n - sb0 : 128) * 400);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(raw_bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         s0 + kAtOffRaw),
+                     "l"(in + sb0), "r"(bytes), "r"(raw_bar)
+                     : "memory");
+    }
+
+    // Tile preparation: the tile's raw records arrived in shared memory (bulk copy
+    // issued during the previous preparation); each word goes to its canonical
+    // position u[k] = lane[(i - k) mod 97] (jump.hpp:32-37) of its state's W row,
+    // the next tile's raw records are fetched, and the rows are extended by the
+    // recurrence. Each thread returns its own row's header (lane 96, i, j, v).
+    const int row = 32 * wq + lane;
+    auto prep = [&](uint64_t tile, uint32_t ph) -> uint4 {
+        const uint64_t sb = tile * 128;
+        const bool live = sb + row < n;
+        const uint64_t rows_here = n - sb < 128 ? n - sb : 128;
+        mbar_wait_a(raw_bar, ph);
+        uint4 hdr = make_uint4(0u, 96u, 32u, 0u);
+        if (live) hdr = raw4[25 * row + 24];
+        const bool ok = !live || state_ok(static_cast<int>(hdr.y), static_cast<int>(hdr.z), hdr.w);
+        const int i0 = ok ? static_cast<int>(hdr.y) : 96;  // clamped so writes stay inside the row
+        bool bad = !ok;
+        if (sub == 0) ci[row] = i0;
+        __syncthreads();
+#pragma unroll 4
+        for (int u = t; u < 128 * 25; u += kAtThreads) {
+            const int st = u / 25, q0 = 4 * (u - 25 * st);  // state, first word
+            const int ri = ci[st];
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            if (static_cast<uint64_t>(st) < rows_here) x = raw4[u];
+            uint32_t* Wr = W + st * kAtWStride;
+            int k = ri - q0;  // canonical index of word q0
+            k += k < 0 ? 97 : 0;
+            Wr[k] = x.x;
+            bad |= x.x > kMask;
+            if (q0 < 96) {
+                k = k == 0 ? 96 : k - 1;
+                Wr[k] = x.y;
+                k = k == 0 ? 96 : k - 1;
+                Wr[k] = x.z;
+                k = k == 0 ? 96 : k - 1;
+                Wr[k] = x.w;
+                bad |= (x.y | x.z | x.w) > kMask;
+            }
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, kStatusBadState);
+        __syncthreads();  // raw staging consumed: fetch the next tile behind this one's work
+        if (t == 0) {
+            const uint64_t nt = tile + gridDim.x;
+            if (nt < n_tiles) {
+                const uint64_t nsb = nt * 128;
+                const uint32_t bytes = static_cast<uint32_t>((n - nsb < 128 ? n - nsb : 128) * 400);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(raw_bar), "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        s0 + kAtOffRaw),
+                    "l"(in + nsb), "r"(bytes), "r"(raw_bar)
+                    : "memory");
+            }
+        }
+        // recurrence extension x_n = x_{n-97} - x_{n-33} into W rows [97, 193): three
+        // rounds of 32 per state (each reads only earlier rounds: n - 33 < lo)
+        for (int it = 0; it < 16; ++it) {
+            uint32_t* Wr = W + (16 * warp + it) * kAtWStride;
+#pragma unroll
+            for (int lo = 97; lo < 193; lo += 32) {
+                const int nn = lo + lane;
+                Wr[nn] = Wr[nn - 97] - Wr[nn - 33];
+                __syncwarp();
+            }
+            if (lane < 3) Wr[193 + lane] = 0u;  // K padding read by the 16-B loads
+        }
+        __syncthreads();
+        return hdr;
+    };
+
+    uint4 hdr_next = make_uint4(0u, 96u, 32u, 0u);
+    if (blockIdx.x < n_tiles) hdr_next = prep(blockIdx.x, 0);
+    // Per tile: pack its rows into TMEM, issue its MMAs, prepare the next tile in
+    // shared memory while the tensor core runs, then read this tile back.
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, phase ^= 1u) {
+        const uint64_t sb = tile * 128;
+        const uint64_t srow = sb + row;
+        const bool live = srow < n;
+        const uint4 hdr = hdr_next;
+        // 2. this thread's row as u8 limbs into TMEM: limb a, K-step ks at tmA + (7 a + ks) 8
+        // (K-steps 0..3 by the first warp of the quarter, 4..6 by the second)
+        {
+            const uint4* Wr4 = reinterpret_cast<const uint4*>(W + row * kAtWStride);
+#pragma unroll 1
+            for (int ks = 4 * sub; ks < (sub ? kAtKSteps : 4); ++ks) {
+                uint32_t v[32];
+#pragma unroll
+                for (int e4 = 0; e4 < 8; ++e4) {
+                    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                    if (8 * ks + e4 < kAtWStride / 4) x = Wr4[8 * ks + e4];
+                    v[4 * e4] = x.x;
+                    v[4 * e4 + 1] = x.y;
+                    v[4 * e4 + 2] = x.z;
+                    v[4 * e4 + 3] = x.w;
+                }
+                uint32_t q[3][8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    limbs3(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], q[0][c], q[1][c], q[2][c]);
+#pragma unroll
+                for (uint32_t a = 0; a < 3; ++a)
+                    asm volatile(
+                        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                            tmA + tq + (a * kAtKSteps + ks) * 8),
+                        "r"(q[a][0]), "r"(q[a][1]), "r"(q[a][2]), "r"(q[a][3]), "r"(q[a][4]), "r"(q[a][5]),
+                        "r"(q[a][6]), "r"(q[a][7])
+                        : "memory");
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // 3. D0 = A0 B0, D1 = A0 B1 + A1 B0, D2 = A0 B2 + A1 B1 + A2 B0 (K = 224 in 7 steps)
+        if (t == 0) {
+            constexpr uint32_t ta[6] = {0, 0, 1, 0, 1, 2}, tb[6] = {0, 1, 0, 2, 1, 0}, td[6] = {0, 1, 1, 2, 2, 2};
+#pragma unroll
+            for (int pq = 0; pq < 6; ++pq) {
+#pragma unroll
+                for (int ks = 0; ks < kAtKSteps; ++ks) {
+                    const uint32_t aa = tmA + (ta[pq] * kAtKSteps + ks) * 8;
+                    const uint64_t db = dB + ((tb[pq] * kAtBPlane + ks * 512) >> 4);
+                    if ((pq == 0 || pq == 1 || pq == 3) && ks == 0)
+                        asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 0;" ::"r"(
+                                         tm + td[pq] * kAtN),
+                                     "r"(aa), "l"(db), "r"(idesc)
+                                     : "memory");
+                    else
+                        asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;" ::"r"(
+                                         tm + td[pq] * kAtN),
+                                     "r"(aa), "l"(db), "r"(idesc)
+                                     : "memory");
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+        }
+        if (tile + gridDim.x < n_tiles) hdr_next = prep(tile + gridDim.x, phase ^ 1u);
+        mbar_wait_a(bar, phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // 4. read back, combine the limbs, decanonicalize (jump.hpp:42-48): column m~
+        // of chunk c is word m~ - 12 -> groups 4 c - 3 + q hold val[4 q .. 4 q + 3]
+        const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(hdr.w) + (kMod - dec)) % kMod);
+        uint4* dst = live ? reinterpret_cast<uint4*>(out[srow].lane) : nullptr;
+#pragma unroll
+        for (int c = 4 * sub; c < (sub ? 7 : 4); ++c) {
+            uint32_t val[16];
+            tc_read_chunk<kAtN>(tm + tq + 16 * c, val);
+            if (dst) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int g = 4 * c - 3 + q;
+                    if (g < 0) continue;
+                    const uint4 x = g == 24 ? make_uint4(val[12], 96u, 32u, v)
+                                            : make_uint4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
+                    __stcs(dst + g, x);
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();  // accumulators and the W rows are free for the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -1147,7 +1414,7 @@ cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t
 }
 
 namespace {
-std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0};
+std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0}, g_cfg_apply_tc{0};
 }  // namespace
 
 // Shared-memory limits of the jump kernels, raised by ranmar_device_setup so no
@@ -1159,8 +1426,22 @@ cudaError_t configure_jump_kernels() {
 }
 
 cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, const uint32_t* P,
-                         uint32_t dec, uint32_t* status, cudaStream_t stream) {
+                         uint32_t dec, uint32_t* status, int sm_count, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
+    // batches of >= 128 states on the tensor cores; RANMAR_APPLY=imad keeps the IMAD
+    // kernel (A/B timing); single jumps (make_streams' first * J) stay on IMAD
+    static const bool use_imad = [] {
+        const char* e = std::getenv("RANMAR_APPLY");
+        return e && e[0] == 'i';
+    }();
+    if (!use_imad && n >= 128) {
+        if (cudaError_t e = ensure_smem(apply_tc_kernel, static_cast<int>(kAtSmem), g_cfg_apply_tc)) return e;
+        const uint64_t tiles = (n + 127) / 128;
+        const uint64_t grid = tiles < uint64_t(sm_count) ? tiles : uint64_t(sm_count);
+        count_launch();
+        apply_tc_kernel<<<static_cast<unsigned>(grid), kAtThreads, kAtSmem, stream>>>(in, out, n, P, dec, status);
+        return cudaGetLastError();
+    }
     if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
     count_launch();
     apply2_kernel<<<static_cast<unsigned>((n + kA2Items - 1) / kA2Items), kA2Threads, kA2Smem,

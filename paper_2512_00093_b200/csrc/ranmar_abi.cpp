@@ -66,7 +66,7 @@ cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*
                              const uint32_t*, cudaStream_t);
 cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
-                         uint32_t*, cudaStream_t);
+                         uint32_t*, int, cudaStream_t);
 cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
                          uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
@@ -534,8 +534,9 @@ int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
     if (rc) return rc;
     const uint32_t dec = arith_dec(mod_u32(from_abi(j), kMod));
     uint32_t* status = nullptr;
-    if (int rc2 = device_status_ptr(&status, nullptr)) return rc2;
-    RB_CUDA(rb::launch_apply(d_in, d_out, n, P, dec, status, s), "apply_kernel launch");
+    int sms = 148;
+    if (int rc2 = device_status_ptr(&status, &sms)) return rc2;
+    RB_CUDA(rb::launch_apply(d_in, d_out, n, P, dec, status, sms, s), "apply_kernel launch");
     return RANMAR_OK;
 }
 
@@ -623,7 +624,7 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     const ranmar_state* a0 = dbase;
     if (first > 0) {
         const uint32_t dec = arith_dec(static_cast<uint32_t>(mulmod(first % kMod, jm, kMod)));
-        RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, status, s), "apply_kernel launch");
+        RB_CUDA(rb::launch_apply(dbase, A0, 1, Pf, dec, status, sms, s), "apply_kernel launch");
         a0 = A0;
     }
     // Levels L-1 .. 1 of the base-128 tree (level 1 writes the anchors'

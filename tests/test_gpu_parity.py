@@ -510,3 +510,21 @@ def test_make_streams_dense_jump_counts_and_determinism(oracle):
             assert got.tobytes() == ref.tobytes()
         assert rb.pow_t_mod_dev(j).cpu().numpy().view(np.uint32).tolist() == \
             oracle.pow_t_mod(j).tolist()
+
+
+@pytest.mark.parametrize("n", [127, 128, 129, 300, 4099])
+def test_batched_jump_tensor_core_path(oracle, n):
+    # batches of >= 128 states run apply_tc_kernel (u8-limb kind::i8 MMAs with the
+    # states' extensions in TMEM); 127 stays on the IMAD kernel: both vs the oracle,
+    # with random cursor phases, a dense jump count and one invalid state flagged
+    base = random_states(n, 1000 + n, oracle)
+    d = rb.states_to_device(base)
+    for j in (2**120, 3**80 + 12345):
+        got = rb.states_to_host(rb.jump_dev(d, j))
+        for k in list(range(0, n, max(1, n // 97))) + [n - 1]:
+            assert got[k:k + 1].tobytes() == oracle.jump_state(base[k:k + 1], j).tobytes(), (n, j, k)
+    assert rb.device_status(clear=True) == 0
+    bad = base.copy()
+    bad["lane"][n // 2, 5] = 1 << 24  # a lane above 24 bits
+    rb.jump_dev(rb.states_to_device(bad), 2**40)
+    assert rb.device_status(clear=True) != 0
