@@ -1129,9 +1129,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
 // groups. The per-tile operand (the states' extensions, u8 limbs) goes to
 // TMEM (168 columns next to the 336 accumulator columns): A from TMEM, B from
 // shared memory, six u8 x u8 -> s32 GEMMs of 128 x 112 x 224 per tile, exact
-// as in bulk_tc_kernel. One 8-warp CTA per SM; warps w and w + 4 share the
-// tile's states 32 w .. 32 w + 31 (their TMEM lane quarter) and split each phase.
-constexpr int kAtThreads = 256;                       // two warps per TMEM lane quarter
+// as in bulk_tc_kernel. One 16-warp CTA per SM; warps w, w + 4, w + 8, w + 12
+// share the tile's states 32 w .. 32 w + 31 (their TMEM lane quarter) and split
+// each phase.
+constexpr int kAtThreads = 512;                       // four warps per TMEM lane quarter
+constexpr int kAtWq = kAtThreads / 128;               // warps per quarter
 constexpr int kAtN = 112;
 constexpr int kAtKSteps = 7;                          // K = 224
 constexpr uint32_t kAtBPlane = 21 * 16 * 16;          // (7 + 14) blocks x 16 shifts x 16 B
@@ -1261,8 +1263,8 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         }
         // recurrence extension x_n = x_{n-97} - x_{n-33} into W rows [97, 193): three
         // rounds of 32 per state (each reads only earlier rounds: n - 33 < lo)
-        for (int it = 0; it < 16; ++it) {
-            uint32_t* Wr = W + (16 * warp + it) * kAtWStride;
+        for (int it = 0; it < 128 / (4 * kAtWq); ++it) {
+            uint32_t* Wr = W + ((128 / (4 * kAtWq)) * warp + it) * kAtWStride;
 #pragma unroll
             for (int lo = 97; lo < 193; lo += 32) {
                 const int nn = lo + lane;
@@ -1285,11 +1287,11 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         const bool live = srow < n;
         const uint4 hdr = hdr_next;
         // 2. this thread's row as u8 limbs into TMEM: limb a, K-step ks at tmA + (7 a + ks) 8
-        // (K-steps 0..3 by the first warp of the quarter, 4..6 by the second)
+        // (K-steps 2 sub, 2 sub + 1 by warp `sub` of the quarter)
         {
             const uint4* Wr4 = reinterpret_cast<const uint4*>(W + row * kAtWStride);
 #pragma unroll 1
-            for (int ks = 4 * sub; ks < (sub ? kAtKSteps : 4); ++ks) {
+            for (int ks = 2 * sub; ks < (2 * sub + 2 < kAtKSteps ? 2 * sub + 2 : kAtKSteps); ++ks) {
                 uint32_t v[32];
 #pragma unroll
                 for (int e4 = 0; e4 < 8; ++e4) {
@@ -1350,7 +1352,7 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(hdr.w) + (kMod - dec)) % kMod);
         uint4* dst = live ? reinterpret_cast<uint4*>(out[srow].lane) : nullptr;
 #pragma unroll
-        for (int c = 4 * sub; c < (sub ? 7 : 4); ++c) {
+        for (int c = 2 * sub; c < (2 * sub + 2 < 7 ? 2 * sub + 2 : 7); ++c) {
             uint32_t val[16];
             tc_read_chunk<kAtN>(tm + tq + 16 * c, val);
             if (dst) {
