@@ -33,7 +33,9 @@ namespace rb {
 namespace {
 
 constexpr int kGT = 64;  // threads (atoms) per block: 24.8 KB of ring, 9 blocks/SM
-constexpr int kBatch = 4;  // accepted pairs per fp64 batch (measured best of 1..8)
+// accepted pairs per fp64 batch. Config 5 with the correctly rounded log (2^24
+// atoms x 300): K = 2..8 -> 25.24 / 23.76 / 23.54 / 22.99 / 22.96 / 23.37 / 23.32 ms
+constexpr int kBatch = 6;
 
 // The ring is the kernel's only shared memory, so it starts at the fixed
 // offset of the CTA's shared window where dynamic shared memory begins (after
