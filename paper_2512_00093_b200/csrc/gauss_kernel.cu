@@ -56,7 +56,12 @@ __device__ __forceinline__ void ring_st(uint32_t off, uint32_t x) {
     asm volatile("st.shared.u32 [%0+1024], %1;" ::"r"(off), "r"(x) : "memory");
 }
 
-template <int K>
+// P > 0: per_step == P with 2K % P == 0 (compile time). When no lane of a warp
+// starts with a cached deviate, every batch of 2K deviates then fills exactly
+// 2K / P whole rows of the output, so its 2K stores address row pointers with
+// immediate column offsets instead of walking the (row, column) countdown per
+// deviate (~6.5 instructions each, ncu source page).
+template <int K, int P>
 __global__ void __launch_bounds__(kGT)
     gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
                     uint64_t steps, double* __restrict__ out, uint32_t* status) {
@@ -148,6 +153,10 @@ __global__ void __launch_bounds__(kGT)
     // once per batch rather than once per pair; then the K independent fp64
     // chains (log, divide, sqrt) are interleaved, so the fp64 pipe sees K-fold
     // instruction-level parallelism instead of one dependent chain per thread.
+    static_assert(P == 0 || (2 * K) % P == 0, "whole rows per batch");
+    constexpr int kRowsPB = P > 0 ? 2 * K / P : 1;
+    const bool rows_fast = P > 0 && __all_sync(__activemask(), q == 0);
+    const uint64_t row_stride = n_atoms * per_step;  // elements between an atom's rows
     while (G - q >= 2 * K) {
         uint32_t a[K], b[K];
         for (int got = 0; got < K;) {
@@ -171,11 +180,25 @@ __global__ void __launch_bounds__(kGT)
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) fac[k] = polar_fac(a[k], b[k]);
+        if (P > 0 && rows_fast) {  // po is at the start of a row
+            double* rp[kRowsPB];
+            rp[0] = po;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            put(__dmul_rn(v2[k], fac[k]));
-            saved = __dmul_rn(v1[k], fac[k]);  // the oracle keeps the last pair's v1 fac
-            put(saved);
+            for (int r = 1; r < kRowsPB; ++r) rp[r] = rp[r - 1] + row_stride;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                st_cs(rp[(2 * k) / (P > 0 ? P : 1)] + (2 * k) % (P > 0 ? P : 1), __dmul_rn(v2[k], fac[k]));
+                saved = __dmul_rn(v1[k], fac[k]);
+                st_cs(rp[(2 * k + 1) / (P > 0 ? P : 1)] + (2 * k + 1) % (P > 0 ? P : 1), saved);
+            }
+            po = rp[kRowsPB - 1] + row_stride;
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                put(__dmul_rn(v2[k], fac[k]));
+                saved = __dmul_rn(v1[k], fac[k]);  // the oracle keeps the last pair's v1 fac
+                put(saved);
+            }
         }
         q += 2 * K;
     }
@@ -298,8 +321,15 @@ cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_
     const int smem = 97 * kGT * 4;  // 24.8 KB: within the default 48 KB limit
     const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
     count_launch();
-    gaussian_kernel<K><<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(
-        d_g, n_atoms, per_step, steps, d_out, status);
+    const dim3 grid(static_cast<unsigned>(blocks));
+    switch (per_step) {  // row-batched stores for the per-step counts that divide 2K
+        case 1: gaussian_kernel<K, 1><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
+        case 2: gaussian_kernel<K, 2><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
+        case 3: gaussian_kernel<K, 3><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
+        case 4: gaussian_kernel<K, 4><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
+        case 6: gaussian_kernel<K, 6><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
+        default: gaussian_kernel<K, 0><<<grid, kGT, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status);
+    }
     return cudaGetLastError();
 }
 

@@ -528,3 +528,21 @@ def test_batched_jump_tensor_core_path(oracle, n):
     bad["lane"][n // 2, 5] = 1 << 24  # a lane above 24 bits
     rb.jump_dev(rb.states_to_device(bad), 2**40)
     assert rb.device_status(clear=True) != 0
+
+
+@pytest.mark.parametrize("per_step,steps", [(1, 25), (2, 13), (3, 100), (3, 7), (4, 7), (6, 5), (6, 3)])
+def test_gaussian_row_batched_stores(oracle, per_step, steps):
+    # per_step dividing 2K: warps whose lanes start without a cached deviate store
+    # whole output rows per batch; a second launch starts from the cache an odd
+    # deviate count leaves (the countdown path), atoms not a multiple of the block
+    from oracle.bind import GAUSS_DTYPE
+    n = 100
+    og = np.zeros(n, GAUSS_DTYPE)
+    og["s"] = random_states(n, 7000 + 10 * per_step + steps, oracle)
+    g = torch.from_numpy(og.copy().view(np.int32).reshape(n, rb.GAUSS_WORDS)).cuda()
+    for _ in range(2):
+        out = rb.gaussian(g, per_step, steps).cpu().numpy()
+        exp = oracle.gaussian_fill(og, per_step, steps)
+        assert ulp_diff(out.reshape(-1), exp.reshape(-1)).max() == 0
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    assert gh.tobytes() == og.tobytes()
