@@ -781,21 +781,35 @@ constexpr uint32_t kTcBPlane = 3584;              // 14 blocks x 16 shifts x 16 
 constexpr uint32_t kTcOffB = 0;                             // 2 buffers x 3 planes
 constexpr uint32_t kTcOffW = kTcOffB + 2 * 3 * kTcBPlane;   // 240 words of w
 constexpr uint32_t kTcOffOut = kTcOffW + 1024;              // kTcStages x 128 records x 400 B
-constexpr int kTcStages = 3;  // record staging buffers: up to 3 bulk stores in flight per SM
-constexpr uint32_t kTcOut = 128 * 400;
-constexpr uint32_t kTcSmem = kTcOffOut + kTcStages * kTcOut;  // 173 KB: one CTA per SM
+// staging buffers: TcLayout (3 x 51 KB of records, or 1 x 98 KB of WMODE rows)
 constexpr uint32_t kTcColT = 3 * 64 + 3 * 48;               // TMEM columns of the T limbs (96)
-static_assert(kTcSmem <= 227 * 1024, "tensor-core bulk smem");
+
 
 struct BulkTcArgs {
     const uint32_t* W1;   // anchors' extensions, H x kWAnchor
     uint64_t H;
-    const uint32_t* Tt;   // [97][128]
+    const uint32_t* Tt;   // the offset table: T[r][k] at Tt[k * tt_cs + r * tt_rs]
+    int tt_rs, tt_cs;
     ranmar_state* out;    // streams [first, first + n)
     uint64_t first, n;
     uint32_t jm;
     const ranmar_state* base;
+    uint32_t* outW;       // WMODE: rows' 193-term extensions (n x kWAnchor) and v
+    uint32_t* outV;
 };
+
+// Staging per anchor: 128 decanonicalised records (400 B) or, in WMODE (the
+// tree's level 1, whose outputs are the next level's anchors), 128 rows of
+// canonical vector + recurrence extension (kWAnchor words).
+template <bool WMODE>
+struct TcLayout {
+    static constexpr uint32_t kRowBytes = WMODE ? 4 * 196 : 400;
+    static constexpr uint32_t kOut = 128 * kRowBytes;
+    static constexpr int kStages = WMODE ? 1 : 3;
+    static constexpr uint32_t kSmem = (2 * 3 * 3584 + 1024) + kStages * kOut;
+};
+static_assert(TcLayout<false>::kSmem <= 227 * 1024 && TcLayout<true>::kSmem <= 227 * 1024,
+              "tensor-core bulk smem");
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
@@ -882,7 +896,9 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
             : "memory");
 }
 
+template <bool WMODE>
 __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_constant__ BulkTcArgs args) {
+    using Lay = TcLayout<WMODE>;
     extern __shared__ __align__(1024) uint32_t tc_smem[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(tc_smem);
     __shared__ uint32_t tmem_base;
@@ -926,7 +942,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
                 const int k = 32 * ks + e;
-                v[e] = k < kPolyN ? args.Tt[k * kRows + r] : 0u;
+                v[e] = k < kPolyN ? args.Tt[k * args.tt_cs + r * args.tt_rs] : 0u;
             }
 #pragma unroll
             for (uint32_t a = 0; a < 3; ++a) {
@@ -978,10 +994,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         const int row = 32 * wq + lane;
         const uint32_t trow = static_cast<uint32_t>(32 * wq) << 16;
         const uint32_t v_base = args.base->v;
-        // w shifted by 3 (sw[n] = w[n - 3]): output column m' = m + 3 is state word
-        // 99 - m', so every 16-column chunk maps onto four whole 16-B record groups
+        // Records: w shifted by 3 (sw[n] = w[n - 3]): output column m' = m + 3 is state
+        // word 99 - m', so every 16-column chunk maps onto four whole 16-B record groups.
+        // WMODE: no shift, column m is canonical word m of the output row.
+        constexpr int kShift = WMODE ? 0 : 3;
         auto load_w = [&](uint64_t hh) -> uint32_t {
-            return hh < args.H && t >= 3 && t < 196 ? args.W1[hh * kWAnchor + t - 3] : 0u;
+            return hh < args.H && t >= kShift && t < 193 + kShift ? args.W1[hh * kWAnchor + t - kShift] : 0u;
         };
         auto store_w = [&](uint32_t w0) {
             if (t < 240) sw[t] = w0;
@@ -1011,6 +1029,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         };
         // chunk c (columns m' = 16 c .. 16 c + 15) of this row -> record groups 24 - 4 c - q
         auto put_chunk = [&](uint8_t* rec, int c, const uint32_t (&val)[16], uint32_t v) {
+            if (WMODE) {  // canonical words 16 c .. 16 c + 15 of the row
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<uint4*>(rec)[4 * c + q] =
+                        make_uint4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
+                return;
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int g = 24 - 4 * c - q;
@@ -1035,7 +1060,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
         build_w(0);
         for (uint32_t i = 0; i < n_anchor; ++i) {
             const uint64_t h = h0 + i * G;
-            const uint32_t sb = i % kTcStages;
+            const uint32_t sb = i % Lay::kStages;
             cbar();  // everyone's build_w has read sw
             if (i + 1 < n_anchor) {
                 store_w(nw);
@@ -1044,12 +1069,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
             }
             nw = load_w(h + 2 * G);
             // this quarter's staging of anchor i - kTcStages has been read by its bulk store
-            if (sub == 0 && lane == 0 && i >= kTcStages)
-                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTcStages - 1) : "memory");
+            if (sub == 0 && lane == 0 && i >= Lay::kStages)
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(Lay::kStages - 1) : "memory");
             qbar();
-            uint8_t* rec = sm + kTcOffOut + sb * kTcOut + 400 * row;
+            uint8_t* rec = sm + kTcOffOut + sb * Lay::kOut + Lay::kRowBytes * row;
             const uint64_t row0 = h * kRows;
-            const bool is_base = args.first == 0 && h == 0 && row == 0;  // stream 0 is the base itself
+            // stream 0 is the base itself (its own cursor layout); WMODE rows are canonical
+            const bool is_base = !WMODE && args.first == 0 && h == 0 && row == 0;
             const uint32_t v = vrow;
             vrow = vrow >= vstep ? vrow - vstep : vrow + (kMod - vstep);  // stream k + 128 G
             // half A: chunks 0..3, two per warp of the quarter
@@ -1086,7 +1112,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
                 uint32_t val[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) val[q] = (d[0][q] + (d[1][q] << 8) + (d[2][q] << 16)) & kMask;
-                if (!is_base) reinterpret_cast<uint4*>(rec)[0] = make_uint4(val[3], val[2], val[1], val[0]);
+                if (WMODE)
+                    reinterpret_cast<uint4*>(rec)[24] = make_uint4(val[0], val[1], val[2], val[3]);  // word 96
+                else if (!is_base)
+                    reinterpret_cast<uint4*>(rec)[0] = make_uint4(val[3], val[2], val[1], val[0]);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             if (is_base && warp == 0) {
@@ -1097,15 +1126,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // records -> bulk copy engine
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(kFreeB));
-            // the quarter's 32 consecutive records (12.8 KB) leave as one bulk store,
-            // issued by its first warp: four stores per anchor, up to kTcStages in flight
+            // the quarter's 32 consecutive rows leave as one bulk store, issued by its
+            // first warp: four stores per anchor, up to kStages in flight
             qbar();
+            if (WMODE) {
+                // rows' recurrence extension u_n = u_{n-97} - u_{n-33}, n = 97 .. 192, in
+                // three rounds of 32 lanes per row (the quarter's 16 + 16 rows), and v
+                if (row0 + row < args.n) args.outV[row0 + row] = v;
+                for (int rr = 16 * sub; rr < 16 * sub + 16; ++rr) {
+                    uint32_t* R = reinterpret_cast<uint32_t*>(sm + kTcOffOut + sb * Lay::kOut +
+                                                              Lay::kRowBytes * (32 * wq + rr));
+#pragma unroll
+                    for (int lo = 97; lo < 193; lo += 32) {
+                        const int nn = lo + lane;
+                        R[nn] = (R[nn - 97] - R[nn - 33]) & kMask;
+                        __syncwarp();
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                qbar();
+            }
             if (sub == 0 && lane == 0) {
                 const uint64_t r0 = row0 + 32 * wq;
                 const uint64_t nr = args.n > r0 ? (args.n - r0 < 32 ? args.n - r0 : 32) : 0;
+                void* dst = WMODE ? static_cast<void*>(args.outW + r0 * kWAnchor) : static_cast<void*>(args.out + r0);
                 if (nr)
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(args.out + r0),
-                                 "r"(s0 + kTcOffOut + sb * kTcOut + 400u * 32u * wq), "r"(static_cast<uint32_t>(nr * 400))
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(s0 + kTcOffOut + sb * Lay::kOut + Lay::kRowBytes * 32u * wq),
+                                 "r"(static_cast<uint32_t>(nr * Lay::kRowBytes))
                                  : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
@@ -1416,14 +1464,18 @@ cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t
 }
 
 namespace {
-std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0}, g_cfg_apply_tc{0};
+std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0}, g_cfg_bulk_tcw{0}, g_cfg_apply_tc{0};
 }  // namespace
 
 // Shared-memory limits of the jump kernels, raised by ranmar_device_setup so no
 // _dev call (or graph capture) has to do it.
 cudaError_t configure_jump_kernels() {
     if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
-    if (cudaError_t e = ensure_smem(bulk_tc_kernel, static_cast<int>(kTcSmem), g_cfg_bulk_tc)) return e;
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kSmem), g_cfg_bulk_tc))
+        return e;
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kSmem), g_cfg_bulk_tcw))
+        return e;
+    if (cudaError_t e = ensure_smem(apply_tc_kernel, static_cast<int>(kAtSmem), g_cfg_apply_tc)) return e;
     return ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk);
 }
 
@@ -1489,16 +1541,33 @@ cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranm
     const uint64_t grid = H < uint64_t(use_imad ? 2 * sm_count : sm_count) ? H
                                                                            : uint64_t(use_imad ? 2 * sm_count : sm_count);
     if (!use_imad) {
-        if (cudaError_t e = ensure_smem(bulk_tc_kernel, static_cast<int>(kTcSmem), g_cfg_bulk_tc)) return e;
-        BulkTcArgs a{W1, H, Tt, out, first, n, jm, d_base};
+        if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kSmem), g_cfg_bulk_tc))
+            return e;
+        BulkTcArgs a{W1, H, Tt, 1, kRows, out, first, n, jm, d_base, nullptr, nullptr};
         count_launch();
-        bulk_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kTcSmem, stream>>>(a);
+        bulk_tc_kernel<false><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<false>::kSmem, stream>>>(a);
         return cudaGetLastError();
     }
     if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk)) return e;
     BulkArgs a{W1, H, Tt, out, first, n, jm, d_base};
     count_launch();
     bulk_kernel<<<static_cast<unsigned>(grid), kBulkThreads, kBulkSmem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+// Level 1 of the stream-start tree on the tensor cores (large trees): rows
+// k = 128 h + r = apply(anchor h, Tab[r]) written as 193-term extensions + v,
+// the bulk kernels' anchors. W: the anchors' extensions; Tab row-major [128][97];
+// v by jump_arith from `src` (the level's source state) with c_lvl = 128^L J mod m.
+cudaError_t launch_level_tc(const uint32_t* W, uint64_t H, const uint32_t* Tab, uint64_t count,
+                            uint32_t c_lvl, const ranmar_state* src, uint32_t* outW, uint32_t* outV,
+                            int sm_count, cudaStream_t stream) {
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kSmem), g_cfg_bulk_tcw))
+        return e;
+    const uint64_t grid = H < uint64_t(sm_count) ? H : uint64_t(sm_count);
+    BulkTcArgs a{W, H, Tab, kPolyN, 1, nullptr, 0, count, c_lvl, src, outW, outV};
+    count_launch();
+    bulk_tc_kernel<true><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<true>::kSmem, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -71,6 +71,8 @@ cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_
                          uint32_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
 cudaError_t launch_copy_state(const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
+cudaError_t launch_level_tc(const uint32_t*, uint64_t, const uint32_t*, uint64_t, uint32_t,
+                            const ranmar_state*, uint32_t*, uint32_t*, int, cudaStream_t);
 cudaError_t launch_bulk(const uint32_t*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
                         uint64_t, uint32_t, const ranmar_state*, int, cudaStream_t);
 cudaError_t configure_jump_kernels();
@@ -254,9 +256,9 @@ Plan plan_for(uint64_t n) {
     o = align256(o + size_t(p.count[1]) * kWAnchor * 4);
     p.off_v1 = o;
     o = align256(o + size_t(p.count[1]) * 4);
-    for (int L = 2; L < p.top; ++L) {
+    for (int L = 2; L < p.top; ++L) {  // level 2 as extension rows (level 1's anchors), above as states
         p.off_lvl[L] = o;
-        o = align256(o + size_t(p.count[L]) * sizeof(ranmar_state));
+        o = align256(o + size_t(p.count[L]) * (L == 2 ? kWAnchor * 4 : sizeof(ranmar_state)));
     }
     p.total = o;
     return p;
@@ -629,15 +631,25 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     }
     // Levels L-1 .. 1 of the base-128 tree (level 1 writes the anchors'
     // extensions for the bulk kernel), then level 0.
+    // With three or more levels, level 2 is written as extension rows and level 1
+    // (up to 2^14 x 128 rows) runs on the tensor cores like level 0.
     const ranmar_state* in = a0;
+    const uint32_t* w2 = nullptr;
     for (int L = p.top - 1; L >= 1; --L) {
         uint64_t pw = 1;  // 128^L mod m
         for (int x = 0; x < L; ++x) pw = pw * 128 % kMod;
         const uint32_t c_lvl = static_cast<uint32_t>(mulmod(pw, jm, kMod));
         const uint64_t count = p.count[L];
         const uint32_t* tab = Tab + size_t(L) * kRows * kPolyN;
-        if (L == 1) {
+        if (L == 1 && w2) {
+            RB_CUDA(rb::launch_level_tc(w2, p.count[2], tab, count, c_lvl, a0, W1, V1, sms, s),
+                    "level_tc launch");
+        } else if (L == 1) {
             RB_CUDA(rb::launch_level(in, count, tab, c_lvl, nullptr, W1, V1, s), "level launch");
+        } else if (L == 2) {
+            uint32_t* o = reinterpret_cast<uint32_t*>(ws + p.off_lvl[L]);
+            RB_CUDA(rb::launch_level(in, count, tab, c_lvl, nullptr, o, V1, s), "level launch");
+            w2 = o;  // (its v row is rewritten by level 1)
         } else {
             ranmar_state* o = reinterpret_cast<ranmar_state*>(ws + p.off_lvl[L]);
             RB_CUDA(rb::launch_level(in, count, tab, c_lvl, o, nullptr, nullptr, s), "level launch");

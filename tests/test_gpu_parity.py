@@ -528,6 +528,10 @@ def test_batched_jump_tensor_core_path(oracle, n):
     bad["lane"][n // 2, 5] = 1 << 24  # a lane above 24 bits
     rb.jump_dev(rb.states_to_device(bad), 2**40)
     assert rb.device_status(clear=True) != 0
+    bad = base.copy()
+    bad["i"][n - 1] = 1000  # a cursor outside the ring: flagged, reads stay inside the record
+    rb.jump_dev(rb.states_to_device(bad), 2**40)
+    assert rb.device_status(clear=True) != 0
 
 
 @pytest.mark.parametrize("per_step,steps", [(1, 25), (2, 13), (3, 100), (3, 7), (4, 7), (6, 5), (6, 3)])
