@@ -326,8 +326,9 @@ __device__ __forceinline__ void extend_items(uint32_t* W, int stride, int items,
     }
 }
 
-// Level kernels process kApplyItems states per CTA (shared-memory Hankel tiles).
-constexpr int kApplyItems = 8;
+// Level kernels process kApplyItems states per CTA (shared-memory Hankel tiles):
+// 8, or 1 for small levels (a tree's top levels: 64 states would be 8 CTAs).
+constexpr int kApplyItemsMax = 8;
 constexpr int kJPad = 104;                        // coefficients padded to 13 x 8
 
 // ---- K3b/K3c for a batch, tiled: out[k] = jump(in[k]) with one shared P.
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kA2Threads, 3)
 // instead of a decanonicalized state.
 constexpr int kWAnchor = 196;  // words per anchor extension row (193 used)
 
-template <bool WMODE>
+template <bool WMODE, int kApplyItems>
 __global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13))
     level_kernel(const ranmar_state* __restrict__ in, uint64_t count,
                  const uint32_t* __restrict__ Tab, uint32_t c_lvl, ranmar_state* __restrict__ out,
@@ -1506,13 +1507,22 @@ cudaError_t launch_apply(const ranmar_state* in, ranmar_state* out, uint64_t n, 
 cudaError_t launch_level(const ranmar_state* in, uint64_t count, const uint32_t* Tab,
                          uint32_t c_lvl, ranmar_state* out, uint32_t* outW, uint32_t* outV,
                          cudaStream_t stream) {
-    const uint64_t blocks = (count + kApplyItems - 1) / kApplyItems;
     count_launch();
+    if (count <= 1024) {  // one state per CTA: the level's latency, not its MACs, matters
+        const unsigned blocks = static_cast<unsigned>(count);
+        if (outW)
+            level_kernel<true, 1><<<blocks, 25, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
+        else
+            level_kernel<false, 1><<<blocks, 13, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
+        return cudaGetLastError();
+    }
+    constexpr int I = kApplyItemsMax;
+    const uint64_t blocks = (count + I - 1) / I;
     if (outW)
-        level_kernel<true><<<static_cast<unsigned>(blocks), kApplyItems * 25, 0, stream>>>(
+        level_kernel<true, I><<<static_cast<unsigned>(blocks), I * 25, 0, stream>>>(
             in, count, Tab, c_lvl, out, outW, outV);
     else
-        level_kernel<false><<<static_cast<unsigned>(blocks), kApplyItems * 13, 0, stream>>>(
+        level_kernel<false, I><<<static_cast<unsigned>(blocks), I * 13, 0, stream>>>(
             in, count, Tab, c_lvl, out, outW, outV);
     return cudaGetLastError();
 }
