@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
 }
 
 // ---- offset tables: Tab_L[r] = P_{r 128^L J} = prod_{b in bits(r)} Q_{7L + b}
-// (warp per entry); Tab_0 also written transposed for the bulk kernel.
+// (warp per entry); Tab_0 and Tab_1 also written transposed for the bulk kernels.
 // One CTA per entry: its <= 6 products run at CTA speed (the chain is the
 // latency of the whole setup, not the few MACs).
 __global__ void __launch_bounds__(256)
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256)
     }
     for (int k = t; k < kPolyN; k += 256) {
         Tab[static_cast<size_t>(e) * kPolyN + k] = acc[k];
-        if (lvl == 0) Tt[k * kRows + r] = acc[k];
+        if (lvl < 2) Tt[static_cast<size_t>(lvl) * kPolyN * kRows + k * kRows + r] = acc[k];
     }
 }
 
@@ -1567,7 +1567,7 @@ cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranm
 
 // Level 1 of the stream-start tree on the tensor cores (large trees): rows
 // k = 128 h + r = apply(anchor h, Tab[r]) written as 193-term extensions + v,
-// the bulk kernels' anchors. W: the anchors' extensions; Tab row-major [128][97];
+// the bulk kernels' anchors. W: the anchors' extensions; Tab transposed [97][128];
 // v by jump_arith from `src` (the level's source state) with c_lvl = 128^L J mod m.
 cudaError_t launch_level_tc(const uint32_t* W, uint64_t H, const uint32_t* Tab, uint64_t count,
                             uint32_t c_lvl, const ranmar_state* src, uint32_t* outW, uint32_t* outV,
@@ -1575,7 +1575,7 @@ cudaError_t launch_level_tc(const uint32_t* W, uint64_t H, const uint32_t* Tab, 
     if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kSmem), g_cfg_bulk_tcw))
         return e;
     const uint64_t grid = H < uint64_t(sm_count) ? H : uint64_t(sm_count);
-    BulkTcArgs a{W, H, Tab, kPolyN, 1, nullptr, 0, count, c_lvl, src, outW, outV};
+    BulkTcArgs a{W, H, Tab, 1, kRows, nullptr, 0, count, c_lvl, src, outW, outV};
     count_launch();
     bulk_tc_kernel<true><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<true>::kSmem, stream>>>(a);
     return cudaGetLastError();

@@ -246,8 +246,8 @@ Plan plan_for(uint64_t n) {
     o = align256(o + kPolyN * 4);
     p.off_tab = o;
     o = align256(o + size_t(p.tab_levels) * kRows * kPolyN * 4);
-    p.off_tt = o;
-    o = align256(o + size_t(kPolyN) * kRows * 4);
+    p.off_tt = o;  // Tab_0 and Tab_1 transposed (the tensor-core kernels' coalesced loads)
+    o = align256(o + 2 * size_t(kPolyN) * kRows * 4);
     p.off_a0 = o;
     o = align256(o + sizeof(ranmar_state));
     p.off_base = o;
@@ -642,7 +642,7 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
         const uint64_t count = p.count[L];
         const uint32_t* tab = Tab + size_t(L) * kRows * kPolyN;
         if (L == 1 && w2) {
-            RB_CUDA(rb::launch_level_tc(w2, p.count[2], tab, count, c_lvl, a0, W1, V1, sms, s),
+            RB_CUDA(rb::launch_level_tc(w2, p.count[2], Tt + size_t(kPolyN) * kRows, count, c_lvl, a0, W1, V1, sms, s),
                     "level_tc launch");
         } else if (L == 1) {
             RB_CUDA(rb::launch_level(in, count, tab, c_lvl, nullptr, W1, V1, s), "level launch");
