@@ -179,6 +179,14 @@ def gather_checksums(sums, world: int):
     return gather_u64(sums, device="cuda")
 
 
+def settle(seconds: float = 1.0) -> None:
+    """Idle before each extra config so it is not timed in the power-capped state the
+    previous config (e.g. config 2's 100 x 16 GiB of stores) left the board in."""
+    import torch
+    torch.cuda.synchronize()
+    time.sleep(seconds)
+
+
 def load_traffic(kernel_key: str):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -451,6 +459,7 @@ def run_ours(args, rank, world, local):
         ctx.close()
 
     # ---- config 1: one stream, seed 12345, 10^8 fp32 uniforms at full width ----
+    settle()
     if not args.quick:
         n1 = 10**8
         s1 = rb.states_to_device(rb.init(12345)).to(dev)
@@ -469,6 +478,7 @@ def run_ours(args, rank, world, local):
         del out1
 
     # ---- config 3: 2^20 stream starts at J = 2^120 (jump-aheads/s) ----
+    settle()
     if not args.quick:
         n3 = C3["n"]
         base3 = rb.init_unchecked(C3["seed"])
@@ -490,6 +500,19 @@ def run_ours(args, rank, world, local):
             step3()
         b.record(stream)
         torch.cuda.synchronize()
+        ms3_direct = max_over_ranks(a.elapsed_time(b) / reps, world)
+        # the same 5 launches captured once in a CUDA graph (the _dev entry points are
+        # capturable) and replayed: the device time without host launch gaps
+        g3 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g3, stream=stream):
+            step3()
+        torch.cuda.synchronize()
+        a.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                g3.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
         ms3 = max_over_ranks(a.elapsed_time(b) / reps, world)
         # generic batched jump: every state jumped by 2^120 (one P_J, 2^20 applies)
         jo = torch.empty_like(st3)
@@ -504,6 +527,8 @@ def run_ours(args, rank, world, local):
         extras["config3"] = {
             "workload": "make_streams(init_unchecked(987654321), 2^120): 2^20 stream starts s_{kJ} per rank",
             "jump_aheads_per_s": n3 * world / (ms3 * 1e-3), "ms": ms3,
+            "timing": "CUDA-graph replay of the make_streams_dev launches (10 reps)",
+            "ms_direct_calls": ms3_direct,
             "batched_jump_state_per_s": n3 * world / (msj * 1e-3), "batched_jump_ms": msj,
             "macs_per_start_bulk": 97 * 97}
         ip = measured_int_peaks()
@@ -551,6 +576,7 @@ def run_ours(args, rank, world, local):
         del st3, ws3, jo, text, off, back, err
 
     # ---- config 4: consume in kernel (no store) ----
+    settle()
     if not args.quick:
         n4 = C4["n"] if not args.c4_streams else args.c4_streams
         st4 = torch.empty((n4, rb.STATE_WORDS), dtype=torch.int32, device=dev)
@@ -595,6 +621,7 @@ def run_ours(args, rank, world, local):
         del st4, ws4, sums4, hist4, all_sums
 
     # ---- config 5: gaussians ----
+    settle()
     if not args.quick:
         n5 = C5["n"]
         st5 = torch.empty((n5, rb.STATE_WORDS), dtype=torch.int32, device=dev)
