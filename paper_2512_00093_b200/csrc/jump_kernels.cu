@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) bulk_kernel(const __grid_cons
 // before that. The CTA's 128 consecutive records (51 KB) leave as ONE TMA
 // bulk store (cp.async.bulk) from a double-buffered staging area.
 constexpr int kTcConsumerWarps = 8;
-constexpr int kTcThreads = 32 * (kTcConsumerWarps + 1);  // + the MMA / bulk-store producer warp
+constexpr int kTcThreads = 32 * (kTcConsumerWarps + 2);  // + one MMA-issuer warp per column half
 constexpr int kTcNA = 64, kTcNB = 48;             // column halves (m < 64, 64 <= m < 112)
 constexpr uint32_t kTcAPlane = 16384;             // 8 K-chunks x 16 row groups x 128 B
 constexpr uint32_t kTcBPlane = 3584;              // 14 blocks x 16 shifts x 16 B
@@ -965,27 +965,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     const uint64_t h0 = blockIdx.x;
     const uint32_t n_anchor = h0 < args.H ? static_cast<uint32_t>((args.H - 1 - h0) / G + 1) : 0u;
 
-    if (warp == kTcConsumerWarps) {
-        // ---------------- producer: one thread issues the MMAs
+    if (warp >= kTcConsumerWarps) {
+        // ---------------- producers: one thread per column half issues its MMAs
+        // (two warps, so the halves' issue sequences run in parallel)
+        const int half = warp - kTcConsumerWarps;
         if (lane == 0 && n_anchor) {
-            const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128);
+            const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128) + (half ? (1024 >> 4) : 0);  // rows m' >= 64: 4 blocks in
             const uint64_t dBbuf = (3 * kTcBPlane) >> 4;  // descriptor step to the other W buffer
-            const uint64_t dBhalf = 1024 >> 4;           // rows m' >= 64 start 4 blocks in
             mbar_wait_a(bar(kWReady), 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tc_issue_half<kTcNA>(tmT, dB0, tmA, bar(kMmaA));
-            tc_issue_half<kTcNB>(tmT, dB0 + dBhalf, tmB, bar(kMmaB));
-            for (uint32_t i = 0; i < n_anchor; ++i) {
+            if (half == 0)
+                tc_issue_half<kTcNA>(tmT, dB0, tmA, bar(kMmaA));
+            else
+                tc_issue_half<kTcNB>(tmT, dB0, tmB, bar(kMmaB));
+            for (uint32_t i = 0; i + 1 < n_anchor; ++i) {
                 const uint32_t nb = (i + 1) & 1;
-                if (i + 1 < n_anchor) {
-                    mbar_wait_a(bar(kWReady + nb), ((i + 1) >> 1) & 1);
-                    mbar_wait_a(bar(kFreeA), i & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                mbar_wait_a(bar(kWReady + nb), ((i + 1) >> 1) & 1);
+                mbar_wait_a(bar(half ? kFreeB : kFreeA), i & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (half == 0)
                     tc_issue_half<kTcNA>(tmT, dB0 + nb * dBbuf, tmA, bar(kMmaA));
-                    mbar_wait_a(bar(kFreeB), i & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    tc_issue_half<kTcNB>(tmT, dB0 + nb * dBbuf + dBhalf, tmB, bar(kMmaB));
-                }
+                else
+                    tc_issue_half<kTcNB>(tmT, dB0 + nb * dBbuf, tmB, bar(kMmaB));
             }
         }
     } else if (n_anchor) {
