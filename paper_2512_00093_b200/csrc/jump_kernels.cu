@@ -797,6 +797,7 @@ struct BulkTcArgs {
     const ranmar_state* base;
     uint32_t* outW;       // WMODE: rows' 193-term extensions (n x kWAnchor) and v
     uint32_t* outV;
+    uint32_t* status;     // kStatusInternal if the smem / TMEM placement assumptions fail
 };
 
 // Staging per anchor: 128 decanonicalised records (400 B) or, in WMODE (the
@@ -808,8 +809,10 @@ struct TcLayout {
     static constexpr uint32_t kOut = 128 * kRowBytes;
     static constexpr int kStages = WMODE ? 1 : 3;
     static constexpr uint32_t kSmem = (2 * 3 * 3584 + 1024) + kStages * kOut;
+    static constexpr uint32_t kLaunchSmem = kSmem + 128;  // + mbarriers and the TMEM base
 };
-static_assert(TcLayout<false>::kSmem <= 227 * 1024 && TcLayout<true>::kSmem <= 227 * 1024,
+constexpr uint32_t kTcSmemBase = 0x400;  // dynamic smem offset in the CTA window (1 KB reserved)
+static_assert(TcLayout<false>::kLaunchSmem <= 227 * 1024 && TcLayout<true>::kLaunchSmem <= 227 * 1024,
               "tensor-core bulk smem");
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -841,6 +844,10 @@ __device__ __forceinline__ uint32_t limb4(uint32_t w0, uint32_t w1, uint32_t w2,
 // (operand B, descriptor dB = limb plane 0 at K-step 0) are read from shared
 // memory. With A in shared memory too, the tensor core's operand reads (276 KB
 // per anchor) saturated the SM's shared-memory bandwidth.
+// Issued by a whole (converged) warp with warp-uniform operands: elect.sync picks
+// the one lane that issues each MMA, and the operands stay in uniform registers
+// (issued from a lane-divergent region instead, every MMA paid an ELECT /
+// R2UR.BROADCAST loop moving its operands to uniform registers, ~15 instructions).
 template <int N>
 __device__ __forceinline__ void tc_issue_half(uint32_t tmT, uint64_t dB, uint32_t tmem, uint32_t bar) {
     constexpr uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (8u << 24);
@@ -851,19 +858,18 @@ __device__ __forceinline__ void tc_issue_half(uint32_t tmT, uint64_t dB, uint32_
         for (int ks = 0; ks < 4; ++ks) {
             const uint32_t ta_addr = tmT + (ta[p] * 4 + ks) * 8;
             const uint64_t db = dB + ((tb[p] * kTcBPlane + ks * 512) >> 4);
-            if ((p == 0 || p == 1 || p == 3) && ks == 0) {  // first product of an accumulator
-                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 0;" ::"r"(tmem + td[p] * N),
-                             "r"(ta_addr), "l"(db), "r"(idesc)
-                             : "memory");
-            } else {
-                asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;" ::"r"(tmem + td[p] * N),
-                             "r"(ta_addr), "l"(db), "r"(idesc)
-                             : "memory");
-            }
+            const uint32_t acc = (p == 0 || p == 1 || p == 3) && ks == 0 ? 0u : 1u;  // first product of a D
+            asm volatile(
+                "{ .reg .pred e, a; elect.sync _|e, 0xffffffff; setp.ne.u32 a, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, a; }" ::"r"(tmem + td[p] * N),
+                "r"(ta_addr), "l"(db), "r"(idesc), "r"(acc)
+                : "memory");
         }
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+    asm volatile(
+        "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar)
+        : "memory");
 }
 
 // 16 columns of this thread's TMEM row starting at column `col` of an
@@ -900,25 +906,32 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
 template <bool WMODE>
 __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_constant__ BulkTcArgs args) {
     using Lay = TcLayout<WMODE>;
+    // All shared memory is dynamic (no static __shared__), so it starts at the fixed
+    // window offset kTcSmemBase and every UMMA descriptor is a compile-time constant
+    // plus a warp-uniform buffer offset (checked on entry). The mbarriers and the
+    // TMEM base live after the staging buffers.
     extern __shared__ __align__(1024) uint32_t tc_smem[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(tc_smem);
-    __shared__ uint32_t tmem_base;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Lay::kSmem);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + Lay::kSmem + 64);
     // mbarriers: MMA half A / B complete (tcgen05.commit), TMEM half A / B drained
-    // (8 consumer warps), W planes of buffer b built (8), records of staging b
-    // written (8), staging b read by its bulk store (the producer)
-    __shared__ __align__(8) uint64_t bars[6];
+    // (8 consumer warps), W planes of buffer b built (8)
     enum { kMmaA = 0, kMmaB = 1, kFreeA = 2, kFreeB = 3, kWReady = 4 };
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
-    const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+    if (s0 != kTcSmemBase) {
+        if (t == 0) atomicOr(args.status, kStatusInternal);
+        return;
+    }
+    const uint32_t b0 = kTcSmemBase + Lay::kSmem;
     auto bar = [&](int k) { return b0 + 8u * static_cast<uint32_t>(k); };
     uint32_t* sw = reinterpret_cast<uint32_t*>(sm + kTcOffW);
     const uint64_t G = gridDim.x;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                         static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -931,8 +944,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tm = tmem_base;
-    const uint32_t tmA = tm, tmB = tm + 3 * kTcNA, tmT = tm + kTcColT;
+    // All 512 columns of one CTA per SM: the allocation starts at column 0, so the
+    // accumulators and the T limbs sit at constant TMEM addresses (checked).
+    const uint32_t tm = *tmem_slot;
+    constexpr uint32_t tmA = 0, tmB = 3 * kTcNA, tmT = kTcColT;
+    const bool tm_ok = tm == 0;
+    if (!tm_ok && t == 0) atomicOr(args.status, kStatusInternal);
     // T limbs into TMEM once per CTA (warps 0-3, one row each): row r, limb a, K-step
     // ks, column c holds limb a of T[r][32 ks + 4 c .. + 3] (coalesced Tt reads)
     if (warp < 4) {
@@ -963,14 +980,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint64_t h0 = blockIdx.x;
-    const uint32_t n_anchor = h0 < args.H ? static_cast<uint32_t>((args.H - 1 - h0) / G + 1) : 0u;
+    const uint32_t n_anchor = h0 < args.H && tm_ok ? static_cast<uint32_t>((args.H - 1 - h0) / G + 1) : 0u;
+    const uint64_t dBase = umma_desc(kTcSmemBase + kTcOffB, 256, 128);  // W planes, buffer 0: a constant
 
     if (warp >= kTcConsumerWarps) {
         // ---------------- producers: one thread per column half issues its MMAs
         // (two warps, so the halves' issue sequences run in parallel)
         const int half = warp - kTcConsumerWarps;
-        if (lane == 0 && n_anchor) {
-            const uint64_t dB0 = umma_desc(s0 + kTcOffB, 256, 128) + (half ? (1024 >> 4) : 0);  // rows m' >= 64: 4 blocks in
+        if (n_anchor) {
+            const uint64_t dB0 = dBase + (half ? (1024 >> 4) : 0);  // rows m' >= 64: 4 blocks in
             const uint64_t dBbuf = (3 * kTcBPlane) >> 4;  // descriptor step to the other W buffer
             mbar_wait_a(bar(kWReady), 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1473,9 +1491,9 @@ std::atomic<uint64_t> g_cfg_apply2{0}, g_cfg_bulk{0}, g_cfg_bulk_tc{0}, g_cfg_bu
 // _dev call (or graph capture) has to do it.
 cudaError_t configure_jump_kernels() {
     if (cudaError_t e = ensure_smem(apply2_kernel, static_cast<int>(kA2Smem), g_cfg_apply2)) return e;
-    if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kSmem), g_cfg_bulk_tc))
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kLaunchSmem), g_cfg_bulk_tc))
         return e;
-    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kSmem), g_cfg_bulk_tcw))
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kLaunchSmem), g_cfg_bulk_tcw))
         return e;
     if (cudaError_t e = ensure_smem(apply_tc_kernel, static_cast<int>(kAtSmem), g_cfg_apply_tc)) return e;
     return ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk);
@@ -1543,7 +1561,7 @@ cudaError_t launch_copy_state(const ranmar_state* src, ranmar_state* dst, uint32
 
 cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
                         uint64_t first, uint64_t n, uint32_t jm, const ranmar_state* d_base,
-                        int sm_count, cudaStream_t stream) {
+                        uint32_t* status, int sm_count, cudaStream_t stream) {
     // tensor-core bulk by default; RANMAR_BULK=imad selects the IMAD kernel (A/B timing)
     static const bool use_imad = [] {
         const char* e = std::getenv("RANMAR_BULK");
@@ -1552,11 +1570,11 @@ cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranm
     const uint64_t grid = H < uint64_t(use_imad ? 2 * sm_count : sm_count) ? H
                                                                            : uint64_t(use_imad ? 2 * sm_count : sm_count);
     if (!use_imad) {
-        if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kSmem), g_cfg_bulk_tc))
+        if (cudaError_t e = ensure_smem(bulk_tc_kernel<false>, static_cast<int>(TcLayout<false>::kLaunchSmem), g_cfg_bulk_tc))
             return e;
-        BulkTcArgs a{W1, H, Tt, 1, kRows, out, first, n, jm, d_base, nullptr, nullptr};
+        BulkTcArgs a{W1, H, Tt, 1, kRows, out, first, n, jm, d_base, nullptr, nullptr, status};
         count_launch();
-        bulk_tc_kernel<false><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<false>::kSmem, stream>>>(a);
+        bulk_tc_kernel<false><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<false>::kLaunchSmem, stream>>>(a);
         return cudaGetLastError();
     }
     if (cudaError_t e = ensure_smem(bulk_kernel, static_cast<int>(kBulkSmem), g_cfg_bulk)) return e;
@@ -1572,13 +1590,13 @@ cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranm
 // v by jump_arith from `src` (the level's source state) with c_lvl = 128^L J mod m.
 cudaError_t launch_level_tc(const uint32_t* W, uint64_t H, const uint32_t* Tab, uint64_t count,
                             uint32_t c_lvl, const ranmar_state* src, uint32_t* outW, uint32_t* outV,
-                            int sm_count, cudaStream_t stream) {
-    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kSmem), g_cfg_bulk_tcw))
+                            uint32_t* status, int sm_count, cudaStream_t stream) {
+    if (cudaError_t e = ensure_smem(bulk_tc_kernel<true>, static_cast<int>(TcLayout<true>::kLaunchSmem), g_cfg_bulk_tcw))
         return e;
     const uint64_t grid = H < uint64_t(sm_count) ? H : uint64_t(sm_count);
-    BulkTcArgs a{W, H, Tab, 1, kRows, nullptr, 0, count, c_lvl, src, outW, outV};
+    BulkTcArgs a{W, H, Tab, 1, kRows, nullptr, 0, count, c_lvl, src, outW, outV, status};
     count_launch();
-    bulk_tc_kernel<true><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<true>::kSmem, stream>>>(a);
+    bulk_tc_kernel<true><<<static_cast<unsigned>(grid), kTcThreads, TcLayout<true>::kLaunchSmem, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -72,9 +72,9 @@ cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_
 cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
 cudaError_t launch_copy_state(const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
 cudaError_t launch_level_tc(const uint32_t*, uint64_t, const uint32_t*, uint64_t, uint32_t,
-                            const ranmar_state*, uint32_t*, uint32_t*, int, cudaStream_t);
+                            const ranmar_state*, uint32_t*, uint32_t*, uint32_t*, int, cudaStream_t);
 cudaError_t launch_bulk(const uint32_t*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
-                        uint64_t, uint32_t, const ranmar_state*, int, cudaStream_t);
+                        uint64_t, uint32_t, const ranmar_state*, uint32_t*, int, cudaStream_t);
 cudaError_t configure_jump_kernels();
 cudaError_t configure_consume_kernel();
 std::atomic<uint64_t> g_launches{0};
@@ -642,7 +642,7 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
         const uint64_t count = p.count[L];
         const uint32_t* tab = Tab + size_t(L) * kRows * kPolyN;
         if (L == 1 && w2) {
-            RB_CUDA(rb::launch_level_tc(w2, p.count[2], Tt + size_t(kPolyN) * kRows, count, c_lvl, a0, W1, V1, sms, s),
+            RB_CUDA(rb::launch_level_tc(w2, p.count[2], Tt + size_t(kPolyN) * kRows, count, c_lvl, a0, W1, V1, status, sms, s),
                     "level_tc launch");
         } else if (L == 1) {
             RB_CUDA(rb::launch_level(in, count, tab, c_lvl, nullptr, W1, V1, s), "level launch");
@@ -656,7 +656,7 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
             in = o;
         }
     }
-    RB_CUDA(rb::launch_bulk(W1, p.count[1], Tt, d_out, first, n, jm, dbase, sms, s),
+    RB_CUDA(rb::launch_bulk(W1, p.count[1], Tt, d_out, first, n, jm, dbase, status, sms, s),
             "bulk_kernel launch");
     return RANMAR_OK;
 }
