@@ -1208,7 +1208,8 @@ constexpr uint32_t kAtBPlane = 21 * 16 * 16;          // (7 + 14) blocks x 16 sh
 constexpr int kAtWStride = 196;                       // 16-B rows: LDS.128 per lane, 4 wavefronts
 constexpr uint32_t kAtOffW = 3 * kAtBPlane;
 constexpr uint32_t kAtOffRaw = kAtOffW + 128 * kAtWStride * 4;  // the next tile's raw records
-constexpr uint32_t kAtSmem = kAtOffRaw + 128 * 400 + 128 * 4;   // + canonical cursors: 168 KB
+constexpr uint32_t kAtOffBar = kAtOffRaw + 128 * 400 + 128 * 4;  // after the canonical cursors
+constexpr uint32_t kAtSmem = kAtOffBar + 64;                      // + 2 mbarriers, TMEM base: 168 KB
 constexpr uint32_t kAtColA = 3 * kAtN;                // TMEM: accumulators, then the A limbs
 
 __global__ void __launch_bounds__(kAtThreads, 1)
@@ -1217,13 +1218,17 @@ __global__ void __launch_bounds__(kAtThreads, 1)
     extern __shared__ __align__(1024) uint32_t at_smem[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(at_smem);
     uint32_t* W = reinterpret_cast<uint32_t*>(sm + kAtOffW);
-    __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) uint64_t mma_bar, raw_bar_s;
+    // all shared memory is dynamic, at the fixed window offset kTcSmemBase (checked),
+    // so the UMMA operands below are constants (see bulk_tc_kernel)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kAtOffBar + 16);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int wq = warp & 3, sub = warp >> 2;  // TMEM lane quarter, which warp of the quarter
     const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
-    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mma_bar));
-    const uint32_t raw_bar = static_cast<uint32_t>(__cvta_generic_to_shared(&raw_bar_s));
+    if (s0 != kTcSmemBase) {
+        if (t == 0) atomicOr(status, kStatusInternal);
+        return;
+    }
+    const uint32_t bar = kTcSmemBase + kAtOffBar, raw_bar = bar + 8;
 
     // B planes from p: item x = 16 b + s holds limbs of pp[16 b + s .. + 15]
     for (int x = t; x < 21 * 16; x += kAtThreads) {
@@ -1242,7 +1247,7 @@ __global__ void __launch_bounds__(kAtThreads, 1)
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                         static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -1255,10 +1260,16 @@ __global__ void __launch_bounds__(kAtThreads, 1)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tm = tmem_base;
-    const uint32_t tmA = tm + kAtColA;
+    // all 512 columns of one CTA per SM: the allocation starts at column 0 (checked)
+    if (*tmem_slot != 0u) {
+        if (t == 0) atomicOr(status, kStatusInternal);
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot) : "memory");
+        return;
+    }
+    constexpr uint32_t tm = 0, tmA = kAtColA;
     const uint32_t tq = static_cast<uint32_t>(32 * wq) << 16;  // this warp's TMEM lane quarter
-    const uint64_t dB = umma_desc(s0, 256, 128);
+    const uint64_t dB = umma_desc(kTcSmemBase, 256, 128);
     constexpr uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(kAtN >> 3) << 17) | (8u << 24);
     const uint64_t n_tiles = (n + 127) / 128;
     uint32_t phase = 0;
@@ -1389,7 +1400,7 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // 3. D0 = A0 B0, D1 = A0 B1 + A1 B0, D2 = A0 B2 + A1 B1 + A2 B0 (K = 224 in 7 steps)
-        if (t == 0) {
+        if (warp == 0) {  // converged warp, elect.sync issues (constant operands)
             constexpr uint32_t ta[6] = {0, 0, 1, 0, 1, 2}, tb[6] = {0, 1, 0, 2, 1, 0}, td[6] = {0, 1, 1, 2, 2, 2};
 #pragma unroll
             for (int pq = 0; pq < 6; ++pq) {
@@ -1397,20 +1408,18 @@ __global__ void __launch_bounds__(kAtThreads, 1)
                 for (int ks = 0; ks < kAtKSteps; ++ks) {
                     const uint32_t aa = tmA + (ta[pq] * kAtKSteps + ks) * 8;
                     const uint64_t db = dB + ((tb[pq] * kAtBPlane + ks * 512) >> 4);
-                    if ((pq == 0 || pq == 1 || pq == 3) && ks == 0)
-                        asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 0;" ::"r"(
-                                         tm + td[pq] * kAtN),
-                                     "r"(aa), "l"(db), "r"(idesc)
-                                     : "memory");
-                    else
-                        asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;" ::"r"(
-                                         tm + td[pq] * kAtN),
-                                     "r"(aa), "l"(db), "r"(idesc)
-                                     : "memory");
+                    const uint32_t acc = (pq == 0 || pq == 1 || pq == 3) && ks == 0 ? 0u : 1u;
+                    asm volatile(
+                        "{ .reg .pred e, a; elect.sync _|e, 0xffffffff; setp.ne.u32 a, %4, 0;\n\t"
+                        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, a; }" ::"r"(tm + td[pq] * kAtN),
+                        "r"(aa), "l"(db), "r"(idesc), "r"(acc)
+                        : "memory");
                 }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                         : "memory");
+            asm volatile(
+                "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar)
+                : "memory");
         }
         if (tile + gridDim.x < n_tiles) hdr_next = prep(tile + gridDim.x, phase ^ 1u);
         mbar_wait_a(bar, phase);
