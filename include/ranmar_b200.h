@@ -199,6 +199,17 @@ int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double*
                         int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
                         int32_t n_types, double tsqrt, int noise, void* stream);
 
+/* The same force update with gaussian noise drawn beforehand: d_noise holds
+ * this step's 3 deviates per atom (n_atoms x 3 f64, e.g. the slice
+ * out + step * 3 n_atoms of one ranmar_gaussian_f64_dev launch with
+ * per_step = 3 over many steps). Equal to ranmar_langevin_dev with
+ * RANMAR_NOISE_GAUSSIAN, step by step, when every atom is in the group at every
+ * step (replaces: the fix-langevin loop of PAPER.md:46-47, repo convention). */
+int ranmar_langevin_noise_dev(uint64_t n_atoms, const double* d_noise, const double* d_v,
+                              double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                              int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
+                              int32_t n_types, double tsqrt, void* stream);
+
 /* Stream bank: n streams transposed slot-major (99 u32 words per stream:
  * 97 ring slots, v, the initial cursor) for consumers that draw the same
  * number of outputs from every stream per launch, so every access of a launch

@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         "ranmar_bank_from_states_dev": (i32, [vp, u64, vp, vp]),
         "ranmar_bank_to_states_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_langevin_bank_dev": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, i32, C.c_double, vp]),
+        "ranmar_langevin_noise_dev": (i32, [u64, vp, vp, vp, vp, vp, i32, vp, vp, i32, C.c_double, vp]),
         "ranmar_langevin_dev": (i32, [vp, u64, vp, vp, vp, vp, i32, vp, vp, i32, C.c_double,
                                       i32, vp]),
         "ranmar_device_status": (i32, [C.POINTER(C.c_uint32), i32]),
@@ -438,6 +439,30 @@ def langevin(gstates, v, f, types, gfactor1, gfactor2, tsqrt: float, noise: int 
                                      None if mask is None else _dptr(mask), groupbit,
                                      _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
                                      float(tsqrt), noise, _stream_ptr(stream)))
+    return f
+
+
+@_on_device
+def langevin_noise(noise, v, f, types, gfactor1, gfactor2, tsqrt: float, mask=None, groupbit: int = 1,
+                   stream=None):
+    """The fix-langevin-style force update with this step's gaussian noise
+    already drawn: noise float64 [n, 3] (e.g. gaussian(g, 3, steps)[step]),
+    f[a, d] += gfactor1[t] * v[a, d] + gfactor2[t] * tsqrt * noise[a, d]
+    (ranmar_langevin_noise_dev). Step by step equal to langevin(...,
+    NOISE_GAUSSIAN) when every atom is in the group at every step."""
+    n = v.shape[0]
+    for t, dt in ((noise, "float64"), (v, "float64"), (f, "float64"), (gfactor1, "float64"),
+                  (gfactor2, "float64")):
+        if str(t.dtype) != "torch." + dt or not t.is_contiguous():
+            raise ValueError("langevin_noise: noise, v, f, gfactor1, gfactor2 must be contiguous float64")
+    if tuple(noise.shape) != (n, 3) or tuple(f.shape) != (n, 3) or types.shape[0] != n:
+        raise ValueError("langevin_noise: noise, v, f must be [n_atoms, 3] and types [n_atoms]")
+    if gfactor1.shape != gfactor2.shape:
+        raise ValueError("langevin_noise: gfactor1 and gfactor2 differ in length")
+    _check(lib().ranmar_langevin_noise_dev(n, _dptr(noise), _dptr(v), _dptr(f), _dptr(types),
+                                           None if mask is None else _dptr(mask), groupbit,
+                                           _dptr(gfactor1), _dptr(gfactor2), gfactor1.shape[0] - 1,
+                                           float(tsqrt), _stream_ptr(stream)))
     return f
 
 

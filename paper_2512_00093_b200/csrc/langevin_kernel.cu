@@ -233,6 +233,51 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
+namespace {
+
+// The same force update with the gaussian noise of this MD step already in HBM
+// (noise[a][d], e.g. one K4 launch's deviates for many steps: gaussian() with
+// 3 calls per atom per step, out[(step * n + a) * 3 + d]). Element-wise, so
+// every access is coalesced (~100 B per atom-step instead of the in-place
+// path's ~450). Equal to ranmar_langevin_dev(NOISE_GAUSSIAN) step by step when
+// every atom is in the group at every step (the noise was drawn for all atoms).
+__global__ void __launch_bounds__(256)
+    langevin_noise_kernel(uint64_t n_atoms, const double* __restrict__ noise,
+                          const double* __restrict__ vel, double* __restrict__ force,
+                          const int32_t* __restrict__ type, const int32_t* __restrict__ mask,
+                          int32_t groupbit, const double* __restrict__ gf1,
+                          const double* __restrict__ gf2, int32_t n_types, double tsqrt,
+                          uint32_t* status) {
+    const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= 3 * n_atoms) return;
+    const uint64_t a = e / 3;
+    if (mask != nullptr && (mask[a] & groupbit) == 0) return;
+    const int32_t t = type[a];
+    if (t < 0 || t > n_types) {
+        if (e % 3 == 0) atomicOr(status, kStatusBadType);
+        return;
+    }
+    const double g1 = gf1[t];
+    const double g2 = __dmul_rn(gf2[t], tsqrt);
+    const double fd = __dadd_rn(__dmul_rn(g1, vel[e]), __dmul_rn(g2, noise[e]));
+    force[e] = __dadd_rn(force[e], fd);
+}
+
+}  // namespace
+
+cudaError_t launch_langevin_noise(uint64_t n_atoms, const double* d_noise, const double* d_v,
+                                  double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                                  int32_t groupbit, const double* d_gf1, const double* d_gf2,
+                                  int32_t n_types, double tsqrt, uint32_t* status,
+                                  cudaStream_t stream) {
+    if (n_atoms == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((3 * n_atoms + 255) / 256);
+    count_launch();
+    langevin_noise_kernel<<<blocks, 256, 0, stream>>>(n_atoms, d_noise, d_v, d_f, d_type, d_mask,
+                                                      groupbit, d_gf1, d_gf2, n_types, tsqrt, status);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_langevin(ranmar_gauss_state* d_g, uint64_t n_atoms, const double* d_v,
                             double* d_f, const int32_t* d_type, const int32_t* d_mask,
                             int32_t groupbit, const double* d_gf1, const double* d_gf2,

@@ -51,6 +51,9 @@ cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, d
 cudaError_t launch_langevin(ranmar_gauss_state*, uint64_t, const double*, double*, const int32_t*,
                             const int32_t*, int32_t, const double*, const double*, int32_t, double,
                             int, uint32_t*, cudaStream_t);
+cudaError_t launch_langevin_noise(uint64_t, const double*, const double*, double*, const int32_t*,
+                                  const int32_t*, int32_t, const double*, const double*, int32_t,
+                                  double, uint32_t*, cudaStream_t);
 cudaError_t launch_bank_from_states(const ranmar_state*, uint64_t, uint32_t*, uint32_t*,
                                    cudaStream_t);
 cudaError_t launch_bank_to_states(const uint32_t*, uint64_t, uint64_t, ranmar_state*, cudaStream_t);
@@ -816,6 +819,21 @@ int ranmar_langevin_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, const double*
                                 d_gfactor2, n_types, tsqrt, noise == RANMAR_NOISE_GAUSSIAN, status,
                                 static_cast<cudaStream_t>(stream)),
             "langevin_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_langevin_noise_dev(uint64_t n_atoms, const double* d_noise, const double* d_v,
+                              double* d_f, const int32_t* d_type, const int32_t* d_mask,
+                              int32_t groupbit, const double* d_gfactor1, const double* d_gfactor2,
+                              int32_t n_types, double tsqrt, void* stream) {
+    if (n_types < 0) return fail(RANMAR_EINVAL, "ranmar_langevin_noise_dev: n_types < 0");
+    if (n_atoms && (!d_noise || !d_v || !d_f || !d_type || !d_gfactor1 || !d_gfactor2))
+        return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    if (n_atoms >= (uint64_t(1) << 62)) return fail(RANMAR_ERANGE, "ranmar_langevin_noise_dev: too many atoms");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_langevin_noise(n_atoms, d_noise, d_v, d_f, d_type, d_mask, groupbit, d_gfactor1,
+                                      d_gfactor2, n_types, tsqrt, status, static_cast<cudaStream_t>(stream)),
+            "langevin_noise_kernel launch");
     return RANMAR_OK;
 }
 

@@ -124,6 +124,8 @@ def test_device_entry_points_validate_arguments_first():
     assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, 1, 1.0, 7, None) == EINVAL
     assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, -1, 1.0, 0, None) == EINVAL
     assert lib.ranmar_langevin_dev(vp, 4, None, vp, vp, None, 1, vp, vp, 1, 1.0, 0, None) == EINVAL
+    assert lib.ranmar_langevin_noise_dev(4, None, vp, vp, vp, None, 1, vp, vp, 1, 1.0, None) == EINVAL
+    assert lib.ranmar_langevin_noise_dev(4, vp, vp, vp, vp, None, 1, vp, vp, -1, 1.0, None) == EINVAL
     s = rb.init(1)
     j = rb._JumpCount()
     assert lib.ranmar_make_streams_dev(s.ctypes.data, C.byref(j), 0, 4, vp, vp, 1 << 20,

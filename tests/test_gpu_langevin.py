@@ -158,3 +158,37 @@ def test_stream_bank_bad_type_keeps_lockstep(oracle):
     s5 = g["s"][5:6].copy()
     oracle.step_n(s5, 3)  # the stream still advanced by 3
     assert back[5:6].tobytes() == s5.tobytes()
+
+
+@pytest.mark.parametrize("n", [37, 4099])
+def test_langevin_with_pregenerated_noise(oracle, n):
+    # one gaussian() launch for all T steps (K4, per_step 3), then one element-wise
+    # consumer per MD step: forces and final states equal the in-place gaussian path
+    # and the oracle step by step (every atom in the group)
+    g, v, f, rng = _atoms(n, 900 + n, oracle, cache_every=5)
+    mass = np.array([0.0, 1.0, 12.011])
+    gf1, gf2 = rb.langevin_factors(mass, t_period=0.1, dt=0.005, noise=rb.NOISE_GAUSSIAN)
+    types = rng.integers(1, 3, n).astype(np.int32)
+    tsqrt = np.sqrt(1.5)
+    steps = 7
+    dv, dt_ = torch.from_numpy(v).cuda(), torch.from_numpy(types).cuda()
+    d1, d2 = torch.from_numpy(gf1).cuda(), torch.from_numpy(gf2).cuda()
+    dg_a, df_a = _dev(g), torch.from_numpy(f.copy()).cuda()  # pre-generated noise
+    dg_b, df_b = _dev(g), torch.from_numpy(f.copy()).cuda()  # in place
+    noise = rb.gaussian(dg_a, 3, steps)                     # [steps, n, 3]
+    fo = f.copy()
+    for step in range(steps):
+        rb.langevin_noise(noise[step], dv, df_a, dt_, d1, d2, tsqrt)
+        rb.langevin(dg_b, dv, df_b, dt_, d1, d2, tsqrt, rb.NOISE_GAUSSIAN)
+        assert oracle.langevin(g, v, fo, types, gf1, gf2, tsqrt, rb.NOISE_GAUSSIAN) == 0
+        assert df_a.cpu().numpy().tobytes() == fo.tobytes(), step
+        assert torch.equal(df_a, df_b), step
+    assert torch.equal(dg_a, dg_b)
+    assert dg_a.cpu().numpy().view(GAUSS_DTYPE).reshape(-1).tobytes() == g.tobytes()
+    assert rb.device_status() == 0
+    # a type outside [0, n_types] is flagged and that atom keeps its force
+    bad = dt_.clone()
+    bad[n // 2] = 9
+    f0 = df_a.clone()
+    rb.langevin_noise(noise[0], dv, df_a, bad, d1, d2, tsqrt)
+    assert rb.device_status(clear=True) != 0 and torch.equal(df_a[n // 2], f0[n // 2])
