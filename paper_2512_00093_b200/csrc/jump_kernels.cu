@@ -288,22 +288,25 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
 __global__ void __launch_bounds__(256)
     tables_kernel(const uint32_t* __restrict__ Q, uint32_t* __restrict__ Tab,
                   uint32_t* __restrict__ Tt) {
+    __shared__ uint32_t f[7][kPolyN];  // the entry's factors, fetched together up front
     __shared__ uint32_t acc[kPolyN];
-    __shared__ uint32_t fac[kPolyN];
     __shared__ BlockMulScratch scr;
     const int e = blockIdx.x, t = threadIdx.x;
     const int lvl = e / kRows, r = e % kRows;
+    // all factor rows in one round of loads (one global latency instead of one per product)
+    for (int x = t; x < 7 * kPolyN; x += 256) {
+        const int b = x / kPolyN, k = x - b * kPolyN;
+        if ((r >> b) & 1) f[b][k] = Q[static_cast<size_t>(7 * lvl + b) * kPolyN + k];
+    }
     int first = -1;  // lowest set bit of r: start from that factor directly
     for (int b = 0; b < 7 && first < 0; ++b)
         if ((r >> b) & 1) first = b;
-    for (int k = t; k < kPolyN; k += 256)
-        acc[k] = first < 0 ? (k == 0) : Q[static_cast<size_t>(7 * lvl + first) * kPolyN + k];
+    __syncthreads();
+    for (int k = t; k < kPolyN; k += 256) acc[k] = first < 0 ? (k == 0) : f[first][k];
     __syncthreads();
     for (int b = first + 1; first >= 0 && b < 7; ++b) {
         if (!((r >> b) & 1)) continue;
-        for (int k = t; k < kPolyN; k += 256) fac[k] = Q[static_cast<size_t>(7 * lvl + b) * kPolyN + k];
-        __syncthreads();
-        block_mulmod(acc, fac, acc, scr);
+        block_mulmod(acc, f[b], acc, scr);
     }
     for (int k = t; k < kPolyN; k += 256) {
         Tab[static_cast<size_t>(e) * kPolyN + k] = acc[k];
