@@ -550,3 +550,17 @@ def test_gaussian_row_batched_stores(oracle, per_step, steps):
         assert ulp_diff(out.reshape(-1), exp.reshape(-1)).max() == 0
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
     assert gh.tobytes() == og.tobytes()
+
+
+@pytest.mark.parametrize("first", [0, 12345, (1 << 40) + 3])
+def test_make_streams_three_level_tree(oracle, first):
+    # n > 128^2: level 2 on the IMAD level kernel, level 1 and level 0 on the tensor
+    # cores, with a stream offset (multi-rank ranges) and a phased base state
+    base = oracle.init(4711)
+    oracle.step_n(base, 40)
+    n = 20000
+    got = rb.states_to_host(rb.make_streams_dev(base, 2**40, n, first=first))
+    for k in (0, 1, 127, 128, 129, 16383, 16384, 16385, n - 1):
+        exp = oracle.make_streams(base, 2**40, 1, first=first + k)
+        assert got[k:k + 1].tobytes() == exp.tobytes(), (first, k)
+    assert rb.device_status(clear=True) == 0
