@@ -55,7 +55,44 @@ __device__ __forceinline__ int line_len(const ranmar_state& s, int line) {
     return 2 + (k + 1 >= 10 ? 2 : 1) + 1 + ndigits(s.lane[k]) + 1;
 }
 
+// "u <k+1> <x>\n" for x < 10^8 without loops or data-dependent branches: the
+// eight decimal digits come from two 4-digit groups by multiply-high, the
+// leading zeros are skipped by predicated byte stores (the generic put_uint
+// loops cost ~4x the instructions, and this line is 97 of every state's 100).
+__device__ __forceinline__ void put_u_line(char* p, uint32_t k1, uint32_t x) {
+    p[0] = 'u';
+    p[1] = ' ';
+    const bool two = k1 >= 10u;
+    const uint32_t kt = k1 / 10u;
+    p[2] = static_cast<char>('0' + (two ? kt : k1));
+    if (two) p[3] = static_cast<char>('0' + (k1 - 10u * kt));
+    char* q = p + (two ? 4 : 3);
+    *q++ = ' ';
+    const int d = ndigits(x);  // 1..8
+    const uint32_t hi = x / 10000u, lo = x - 10000u * hi;
+    uint32_t dig[8];
+    {
+        const uint32_t h1 = hi / 100u, h0 = hi - 100u * h1, l1 = lo / 100u, l0 = lo - 100u * l1;
+        const uint32_t g[4] = {h1, h0, l1, l0};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t t = g[c] / 10u;
+            dig[2 * c] = t;
+            dig[2 * c + 1] = g[c] - 10u * t;
+        }
+    }
+    char* z = q - (8 - d);  // digit i of the 8 lands at z + i
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (i >= 8 - d) z[i] = static_cast<char>('0' + dig[i]);
+    q[d] = '\n';
+}
+
 __device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* p) {
+    if (line >= 3) {
+        put_u_line(p, static_cast<uint32_t>(line - 2), s.lane[line - 3]);
+        return;
+    }
     if (line == 0) {
         const char m[] = "ranmar24 v1\n";
         for (int c = 0; c < 12; ++c) p[c] = m[c];
@@ -184,23 +221,27 @@ __global__ void __launch_bounds__(32 * kTTStates)
     const uint64_t kend = k0 + kTTStates < n ? k0 + kTTStates : n;
     const uint64_t g0 = off[k0], g1 = off[kend];
     const uint32_t shift = static_cast<uint32_t>(g0 & 15);
-    if (k < n && off[k + 1] != off[k]) {  // (invalid states have empty texts)
-        const ranmar_state& s = st[k];
-        char* base = stage + shift + (off[k] - g0);
-        uint32_t before = 0;  // bytes of the lines of previous passes
+    // (invalid states have empty texts). The warp-uniform condition predicates the
+    // work instead of branching around it: the shuffles then run in converged code
+    // (behind a branch ptxas cannot prove uniform they become WARPSYNC/collective
+    // loops).
+    const bool act = k < n && off[k + 1] != off[k];
+    const ranmar_state& s = st[act ? k : k0];
+    char* base = stage + shift + (act ? off[k] - g0 : 0);
+    uint32_t before = 0;  // bytes of the lines of previous passes
 #pragma unroll
-        for (int pass = 0; pass < 4; ++pass) {
-            const int line = pass * 32 + l;
-            const uint32_t len = line < 100 ? static_cast<uint32_t>(line_len(s, line)) : 0u;
-            uint32_t incl = len;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int line = pass * 32 + l;
+        const bool mine = act && line < 100;
+        const uint32_t len = mine ? static_cast<uint32_t>(line_len(s, line)) : 0u;
+        uint32_t incl = len;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (l >= o) incl += y;
-            }
-            if (line < 100) put_line(s, line, base + before + incl - len);
-            before += __shfl_sync(0xffffffffu, incl, 31);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (l >= o) incl += y;
         }
+        if (mine) put_line(s, line, base + before + incl - len);
+        before += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncthreads();
     const uint64_t a = (g0 + 15) & ~uint64_t(15), b = g1 & ~uint64_t(15);
