@@ -24,7 +24,6 @@
 // whatever the (diverged) cursors. States are moved between HBM and the ring
 // with 16-B vector accesses (the 416-B records are 16-B aligned).
 #include <cstdint>
-#include <cstdlib>
 #include <type_traits>
 
 #include "gauss_math.cuh"
@@ -35,8 +34,11 @@ namespace rb {
 namespace {
 
 constexpr int kGT = 64;  // threads (atoms) per block: 24.8 KB of ring, 9 blocks/SM
-// accepted pairs per fp64 batch. Config 5 with the correctly rounded log (2^24
-// atoms x 300): K = 2..8 -> 25.24 / 23.76 / 23.54 / 22.99 / 22.96 / 23.37 / 23.32 ms
+// accepted pairs per fp64 batch. Config 5 (2^24 atoms x 300, per_step 3), with
+// the pipelined ring loads and the split log: K = 3 (row-batched stores, 96
+// registers, 9 blocks/SM) 20.30 ms; K = 6 (row-batched, 128 registers, 8
+// blocks/SM) 21.30; K = 4 / 5 (per_step 3 does not divide 2K: countdown
+// stores) 21.36 / 21.31; K = 8 22.05.
 constexpr int kBatch = 3;
 
 // The ring is the kernel's only shared memory, so it starts at the fixed
@@ -268,570 +270,7 @@ __global__ void __launch_bounds__(kGT)
     gs->has_saved = has ? 1u : 0u;
 }
 
-// ------------------------------------------------------------------ K4p
-// Thread per atom with a warp-wide pool of accepted pairs. Every lane keeps
-// drawing attempt pairs on its own ring until its atom has all the pairs this
-// launch needs; accepted pairs enter the warp's FIFO pool in shared memory in
-// order (ballot + popc), tagged with the owning lane, its cached-deviate bit
-// and the low 8 bits of the atom's pair index. Once the pool holds 32 K pairs
-// the warp takes them, K per lane, whatever atoms they belong to, and runs the
-// K fp64 chains: no lane waits for another lane's rejections (the batch-of-K
-// attempt loop above idles ~1/3 of its lane slots), and no accepted pair is
-// shifted through registers. A pair's full index is the owning lane's current
-// pair count minus its distance (< 256) in the pool; its deviates go to output
-// slots 2 j + has, 2 j + 1 + has of the atom, i.e. rows (2 j + has) / P. The
-// pair that completes an atom also leaves its v1 fac as the atom's cache.
-// Requires steps * per_step < 2^32 and per_step == P (the launcher routes
-// other shapes to K4w).
-template <int K>
-struct K4pShape {
-    static constexpr int CAP = 32 * K + 32;  // >= 32 K + 31 queued pairs
-    static_assert(CAP <= 256, "pair indices are tagged mod 256");
-    static constexpr uint32_t kPoolBase = kRingBase + 97 * kGT * 4;
-    static constexpr int smem = 97 * kGT * 4 + (kGT / 32) * CAP * 8;
-};
-
-__device__ __forceinline__ void pool_st(uint32_t addr, uint32_t a, uint32_t b) {
-    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
-__device__ __forceinline__ void pool_ld(uint32_t addr, uint32_t& a, uint32_t& b) {
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(addr));
-}
-
-template <int K, int P>
-__global__ void __launch_bounds__(kGT)
-    gaussian_pool_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint32_t G,
-                         double* __restrict__ out, uint32_t* status) {
-    using Sh = K4pShape<K>;
-    constexpr int CAP = Sh::CAP;
-    extern __shared__ uint32_t ring[];  // [97][kGT], then the warps' pools
-    const int t = threadIdx.x, l = t & 31, w = t >> 5;
-    if (static_cast<uint32_t>(__cvta_generic_to_shared(ring)) != kRingBase) {
-        if (t == 0) atomicOr(status, kStatusInternal);
-        return;
-    }
-    const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kGT + w * 32;  // atom of lane 0
-    const uint64_t atom = wbase + l;
-    bool live = atom < n_atoms;
-    ranmar_gauss_state* gs = g + (live ? atom : 0);
-    int i0 = 0;
-    uint32_t v = 0, has = 0;
-    if (live) {
-        i0 = gs->s.i;
-        v = gs->s.v;
-        if (!state_ok(i0, gs->s.j, v)) {
-            atomicOr(status, kStatusBadState);
-            live = false;
-        }
-    }
-    constexpr uint32_t kSlot = 4 * kGT;
-    const uint32_t top = 4 * t + 96 * kSlot;
-    uint32_t ai = 4 * t + i0 * kSlot;
-    uint32_t aj = 4 * t + (i0 >= 64 ? i0 - 64 : i0 + 33) * kSlot;
-    uint32_t T = 0;  // pairs this atom needs: ceil((G - has) / 2)
-    if (live) {
-        const uint4* src = reinterpret_cast<const uint4*>(gs->s.lane);
-#pragma unroll 4
-        for (int q = 0; q < 24; ++q) {
-            const uint4 x = src[q];
-            ring[(4 * q + 0) * kGT + t] = x.x;
-            ring[(4 * q + 1) * kGT + t] = x.y;
-            ring[(4 * q + 2) * kGT + t] = x.z;
-            ring[(4 * q + 3) * kGT + t] = x.w;
-        }
-        ring[96 * kGT + t] = gs->s.lane[96];
-        has = gs->has_saved != 0 ? 1u : 0u;
-        if (has) st_cs(out + atom * P, gs->saved);  // output 0: the cached deviate
-        T = (G - has + 1) / 2;
-    }
-    auto attempt = [&](uint32_t& u0, uint32_t& u1) -> bool {
-        uint32_t u[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t x = ring_ld(ai) - ring_ld(aj);
-            ring_st(ai, x);
-            ai = min(ai - kSlot, top);
-            aj = min(aj - kSlot, top);
-            v = add_mod_m(v, kStepA);
-            u[h] = (x - v) & kMask;
-        }
-        const int32_t da = static_cast<int32_t>(u[0]) - (1 << 23);
-        const int32_t db = static_cast<int32_t>(u[1]) - (1 << 23);
-        const int64_t s = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
-        u0 = u[0];
-        u1 = u[1];
-        return s > 0 && s < (int64_t(1) << 46);
-    };
-    const uint32_t pbase = Sh::kPoolBase + w * CAP * 8;
-    const uint32_t tag = (static_cast<uint32_t>(l) << 24) | (has << 29);
-    const uint32_t lt = (1u << l) - 1u;
-    const uint64_t rowstride = n_atoms * P;
-    uint32_t enq = 0;                  // pairs this lane has queued
-    uint32_t head = 0, tail = 0, cnt = 0;  // the warp's pool (warp-uniform)
-    for (;;) {
-        while (cnt < 32 * K) {
-            const bool act = enq < T;
-            if (!__any_sync(0xffffffffu, act)) break;
-            uint32_t u0 = 0, u1 = 0;
-            const bool acc = act && attempt(u0, u1);
-            const uint32_t bal = __ballot_sync(0xffffffffu, acc);
-            if (acc) {
-                uint32_t slot = tail + __popc(bal & lt);
-                slot = slot >= CAP ? slot - CAP : slot;
-                pool_st(pbase + slot * 8, u0 | tag, u1 | (enq << 24));
-                ++enq;
-            }
-            const uint32_t nb = __popc(bal);
-            tail += nb;
-            tail = tail >= CAP ? tail - CAP : tail;
-            cnt += nb;
-        }
-        if (cnt == 0) break;
-        const uint32_t take = min(cnt, static_cast<uint32_t>(32 * K));
-        uint32_t w0[K], w1[K], pid[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t idx = 32 * k + l;
-            uint32_t slot = head + idx;
-            slot = slot >= CAP ? slot - CAP : slot;
-            // a lane without a pair computes an accepted dummy (v1 = 1/2, v2 = 0)
-            w0[k] = 0xC00000u | (static_cast<uint32_t>(l) << 24);
-            w1[k] = 0x800000u;
-            if (idx < take) pool_ld(pbase + slot * 8, w0[k], w1[k]);
-            const uint32_t e = __shfl_sync(0xffffffffu, enq, (w0[k] >> 24) & 31);
-            pid[k] = e - 1 - ((e - 1 - (w1[k] >> 24)) & 255);
-        }
-        double rsq[K], lg[K];
-        bool all_ok = true;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            rsq[k] = polar_rsq(w0[k] & kMask, w1[k] & kMask);
-            bool ok;
-            lg[k] = crlog_fast(rsq[k], ok);
-            all_ok = all_ok && ok;
-        }
-        if (__builtin_expect(!all_ok, 0)) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                bool ok;
-                crlog_fast(rsq[k], ok);
-                if (!ok) lg[k] = crlog_accurate(rsq[k]).y;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const double fac = polar_fac_of(rsq[k], lg[k]);
-            const double d2 = __dmul_rn(polar_v(w1[k] & kMask), fac);
-            const double d1 = __dmul_rn(polar_v(w0[k] & kMask), fac);
-            if (32 * k + l < take) {
-                const uint32_t a = (w0[k] >> 24) & 31, ha = (w0[k] >> 29) & 1;
-                const uint32_t q = 2 * pid[k] + ha;
-                const uint32_t row = q / P, col = q - row * P;
-                double* po = out + row * rowstride + (wbase + a) * P + col;
-                st_cs(po, d2);
-                if (q + 1 < G) st_cs(col + 1 < P ? po + 1 : po + (rowstride - (P - 1)), d1);
-                if (pid[k] == (G - ha - 1) / 2) g[wbase + a].saved = d1;  // the atom's last pair
-            }
-        }
-        head += take;
-        head = head >= CAP ? head - CAP : head;
-        cnt -= take;
-    }
-    if (!live) return;
-    {
-        uint4* dst = reinterpret_cast<uint4*>(gs->s.lane);
-#pragma unroll 4
-        for (int qq = 0; qq < 24; ++qq)
-            dst[qq] = make_uint4(ring[(4 * qq + 0) * kGT + t] & kMask, ring[(4 * qq + 1) * kGT + t] & kMask,
-                                 ring[(4 * qq + 2) * kGT + t] & kMask, ring[(4 * qq + 3) * kGT + t] & kMask);
-    }
-    const int i = static_cast<int>((ai - 4 * t) / kSlot);
-    *reinterpret_cast<uint4*>(gs->s.lane + 96) =
-        make_uint4(ring[96 * kGT + t] & kMask, static_cast<uint32_t>(i),
-                   static_cast<uint32_t>(i >= 64 ? i - 64 : i + 33), v);
-    gs->has_saved = (G - has) & 1u;
-}
-
-// ------------------------------------------------------------------ K4w
-// Warp-cooperative gaussian(): each warp owns A atoms of a CTA tile of
-// T = kWW * A atoms, and the output is produced in chunks of CH = 64 PL
-// deviates per atom.
-//   generation  two rounds of the K1 warp mapping (gen_kernels.cu) give 64
-//               consecutive uniforms of one atom = 32 attempt pairs, one per
-//               lane; the exact integer test 0 < s < 2^46 runs on every lane
-//               and accepted pairs enter the atom's queue in order (ballot +
-//               popc). No lane waits for another lane's rejections.
-//   fp64        each lane takes pair j = 32 p + l (p < PL) of each of its A
-//               atoms: A * PL independent log / divide / sqrt chains per lane,
-//               every lane busy.
-//   output      deviates land in a shared-memory stage [atom][slot] (slot =
-//               output index - chunk start), then the CTA writes the chunk's
-//               output rows: per step row the tile's atoms are contiguous
-//               (T * per_step doubles), so the stores are coalesced although
-//               every atom's deviates are strided by n_atoms * per_step.
-// The stage is double-buffered, so one barrier per chunk separates the fp64
-// writes of chunk c from its write-out and the write-out of chunk c - 1 from
-// the fp64 writes of chunk c + 1.
-// Pairs always start at even uniform offsets from the launch's start state (a
-// rejected attempt consumes both uniforms; a cached deviate consumes none),
-// so pair j of an atom = (u_{2a}, u_{2a+1}) for its j-th accepted attempt a.
-// An atom with a cached deviate (has = 1) emits it as output 0, so pair j
-// fills output slots 2 j + has, 2 j + 1 + has; the pair that straddles a chunk
-// boundary leaves its second deviate as the next chunk's slot 0, which is the
-// atom's running `saved` value (the oracle's cache, kept in a register).
-// The last pair any atom needs comes from the last generation it ran (a
-// generation runs only while the queue holds fewer pairs than the chunk
-// needs), so the atom stops at uniform n in (64 g - 64, 64 g] after g
-// generations and its ring window [n - 97, n) is among the last five rounds.
-constexpr int kWW = 4;  // warps per CTA
-
-template <int A, int PL, int P>
-struct K4wShape {
-    static constexpr int T = kWW * A;        // atoms per CTA tile
-    static constexpr int CH = 64 * PL;       // output slots per atom per chunk
-    static constexpr int QCAP = (PL == 1) ? 64 : 128;  // >= 32 PL + 31 queued pairs
-    // stage row stride (doubles): >= CH + 1 (the straddling pair's dropped
-    // second deviate) and == per_step mod 16, so that the write-out's LDS.64
-    // of consecutive (atom, column) elements hit distinct banks
-    static constexpr int S = (P > 0) ? CH + 1 + ((P - 1) % 16) : CH + 1;
-    static constexpr size_t smem = sizeof(double) * 2 * T * S + sizeof(uint64_t) * T * QCAP;
-};
-
-constexpr uint64_t kK4wDummy = (0xC00000ull) | (0x800000ull << 24);
-
-// Per-atom generator registers (the K1 mapping with a fifth round kept).
-struct K4wGen {
-    uint32_t R1, R2, R3, R4, R5, prev, V;
-};
-
-template <int A, int PL, int P>
-__global__ void __launch_bounds__(32 * kWW)
-    gaussian_warp_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
-                         uint64_t steps, double* __restrict__ out, uint32_t* status) {
-    using Sh = K4wShape<A, PL, P>;
-    constexpr int T = Sh::T, CH = Sh::CH, QCAP = Sh::QCAP, S = Sh::S;
-    extern __shared__ __align__(16) unsigned char k4w_smem[];
-    double* stage = reinterpret_cast<double*>(k4w_smem);                          // [2][T][S]
-    uint64_t* queue = reinterpret_cast<uint64_t*>(k4w_smem + sizeof(double) * 2 * T * S);  // [T][QCAP]
-
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t a0 = static_cast<uint64_t>(blockIdx.x) * T;
-    const uint64_t ps = P > 0 ? static_cast<uint64_t>(P) : per_step;
-    const uint64_t G = steps * ps;
-    const int src = (l + 31) & 31;
-    const uint32_t A32 = static_cast<uint32_t>((32ull * kStepA) % kMod);
-
-    K4wGen gen[A];
-    uint32_t qhead[A], qtail[A], llast[A];
-    uint64_t gens[A], total[A];
-    double saved[A];
-    int has0[A];
-    bool act[A];
-    uint32_t amask = 0;  // this warp's active atoms (bit k)
-#pragma unroll
-    for (int k = 0; k < A; ++k) {
-        const uint64_t atom = a0 + w * A + k;
-        act[k] = false;
-        has0[k] = 0;
-        saved[k] = 0.0;
-        qhead[k] = qtail[k] = llast[k] = 0;
-        gens[k] = total[k] = 0;
-        gen[k] = K4wGen{0, 0, 0, 0, 0, 0, 0};
-        if (atom < n_atoms) {
-            const ranmar_gauss_state* gs = g + atom;
-            const int i0 = gs->s.i, j0 = gs->s.j;
-            const uint32_t v0 = gs->s.v;
-            if (!state_ok(i0, j0, v0)) {
-                if (l == 0) atomicOr(status, kStatusBadState);
-            } else {
-                act[k] = true;
-                const uint32_t* lane = gs->s.lane;
-                K4wGen& s = gen[k];
-                s.R1 = lane[(i0 + 32 - l) % 97];
-                s.R2 = lane[(i0 + 64 - l) % 97];
-                s.R3 = lane[(i0 + 96 - l) % 97];
-                s.R4 = (l == 31) ? lane[i0] : 0u;
-                s.R5 = 0;
-                s.V = arith_advance(v0, static_cast<uint64_t>(l) + 1);
-                has0[k] = gs->has_saved != 0 ? 1 : 0;
-                saved[k] = gs->saved;
-                // pairs this launch needs: ceil((G - has) / 2)
-                total[k] = (G - has0[k] + 1) / 2;
-            }
-        }
-        gen[k].prev = __shfl_sync(0xffffffffu, gen[k].R4 - gen[k].R2, src);
-        amask |= act[k] ? (1u << k) : 0u;
-    }
-    // the tile's active atoms (bit w * A + k), for the write-out
-    __shared__ uint32_t s_tmask[kWW];
-    if (l == 0) s_tmask[w] = amask;
-    __syncthreads();
-    uint32_t tmask = 0;
-#pragma unroll
-    for (int ww = 0; ww < kWW; ++ww) tmask |= s_tmask[ww] << (ww * A);
-
-    // write-out position of this thread when a tile row (T * per_step doubles)
-    // fits the CTA: rpi rows per pass, element wi = (atom a, column col)
-    const uint64_t rowlen64 = static_cast<uint64_t>(T) * ps;
-    const bool fixed = rowlen64 <= 32 * kWW;
-    const uint32_t rowlen = fixed ? static_cast<uint32_t>(rowlen64) : 1u;
-    const uint32_t rpi = (32 * kWW) / rowlen;
-    const uint32_t rr0 = threadIdx.x / rowlen, wi = threadIdx.x - rr0 * rowlen;
-    const uint32_t a = fixed ? wi / static_cast<uint32_t>(ps) : 0u;
-    const uint32_t col = wi - a * static_cast<uint32_t>(ps);
-    const bool wact = fixed && rr0 < rpi && ((tmask >> a) & 1u);
-    const uint64_t rowstride = n_atoms * ps;
-
-    const uint64_t nch = (G + CH - 1) / CH;
-    for (uint64_t c = 0; c < nch; ++c) {
-        double* stg = stage + (c & 1) * (T * S);
-        const uint64_t q0 = c * CH;
-        const uint64_t q1 = min(q0 + CH, G);
-        // generation: fill every active atom's queue to this chunk's need
-        uint32_t need[A];
-#pragma unroll
-        for (int k = 0; k < A; ++k) {
-            need[k] = 0;
-            if (!act[k]) continue;
-            const uint64_t pc = min((q1 - has0[k] + 1) / 2, total[k]);  // pairs through this chunk
-            const uint64_t p0 = min((q0 - has0[k] + 1) / 2, total[k]);
-            need[k] = static_cast<uint32_t>(pc - p0);
-            uint64_t* qk = queue + (w * A + k) * QCAP;
-            K4wGen& s = gen[k];
-            while (qtail[k] - qhead[k] < need[k]) {
-                uint32_t uab[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t X = __shfl_sync(0xffffffffu, s.R3 - s.R1, src);
-                    const uint32_t y = (l == 0) ? s.prev : X;
-                    s.prev = X;
-                    s.R5 = s.R4;
-                    s.R4 = s.R3;
-                    s.R3 = s.R2;
-                    s.R2 = s.R1;
-                    s.R1 = y;
-                    uab[h] = (y - s.V) & kMask;
-                    s.V = add_mod_m(s.V, A32);
-                }
-                const int s1 = (2 * l) & 31;  // attempt l = uniforms 2l, 2l + 1 of the 64
-                const uint32_t x1 = __shfl_sync(0xffffffffu, uab[0], s1);
-                const uint32_t y1 = __shfl_sync(0xffffffffu, uab[1], s1);
-                const uint32_t x2 = __shfl_sync(0xffffffffu, uab[0], s1 + 1);
-                const uint32_t y2 = __shfl_sync(0xffffffffu, uab[1], s1 + 1);
-                const uint32_t u1 = l < 16 ? x1 : y1, u2 = l < 16 ? x2 : y2;
-                const int32_t da = static_cast<int32_t>(u1) - (1 << 23);
-                const int32_t db = static_cast<int32_t>(u2) - (1 << 23);
-                const int64_t sq = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
-                const bool acc = sq > 0 && sq < (int64_t(1) << 46);
-                const uint32_t bal = __ballot_sync(0xffffffffu, acc);
-                if (acc) {
-                    const uint32_t slot = (qtail[k] + __popc(bal & ((1u << l) - 1u))) & (QCAP - 1);
-                    qk[slot] = static_cast<uint64_t>(u1) | (static_cast<uint64_t>(u2) << 24) |
-                               (static_cast<uint64_t>(l) << 48);
-                }
-                qtail[k] += __popc(bal);
-                ++gens[k];
-            }
-        }
-        __syncwarp();
-        // fp64: pair j = 32 p + l of each atom
-        uint64_t e[A][PL];
-#pragma unroll
-        for (int k = 0; k < A; ++k) {
-            const uint64_t* qk = queue + (w * A + k) * QCAP;
-#pragma unroll
-            for (int p = 0; p < PL; ++p) {
-                const uint32_t j = 32 * p + l;
-                // a lane without a pair computes an accepted dummy (v1 = 1/2, v2 = 0)
-                e[k][p] = j < need[k] ? qk[(qhead[k] + j) & (QCAP - 1)] : kK4wDummy;
-            }
-        }
-        // the fast log of every chain first, the rare accurate phase after all
-        // of them (one branch), then the divides and square roots
-        double rsq[A][PL], lg[A][PL];
-        bool all_ok = true;
-#pragma unroll
-        for (int k = 0; k < A; ++k) {
-#pragma unroll
-            for (int p = 0; p < PL; ++p) {
-                const uint32_t u1 = static_cast<uint32_t>(e[k][p]) & kMask;
-                const uint32_t u2 = static_cast<uint32_t>(e[k][p] >> 24) & kMask;
-                rsq[k][p] = polar_rsq(u1, u2);
-                bool ok;
-                lg[k][p] = crlog_fast(rsq[k][p], ok);
-                all_ok = all_ok && ok;
-            }
-        }
-        if (__builtin_expect(!all_ok, 0)) {
-#pragma unroll
-            for (int k = 0; k < A; ++k) {
-#pragma unroll
-                for (int p = 0; p < PL; ++p) {
-                    bool ok;
-                    crlog_fast(rsq[k][p], ok);
-                    if (!ok) lg[k][p] = crlog_accurate(rsq[k][p]).y;
-                }
-            }
-        }
-        double d1[A][PL], d2[A][PL];
-#pragma unroll
-        for (int k = 0; k < A; ++k) {
-#pragma unroll
-            for (int p = 0; p < PL; ++p) {
-                const uint32_t u1 = static_cast<uint32_t>(e[k][p]) & kMask;
-                const uint32_t u2 = static_cast<uint32_t>(e[k][p] >> 24) & kMask;
-                const double fac = polar_fac_of(rsq[k][p], lg[k][p]);
-                d2[k][p] = __dmul_rn(polar_v(u2), fac);
-                d1[k][p] = __dmul_rn(polar_v(u1), fac);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < A; ++k) {
-            double* sk = stg + (w * A + k) * S;
-            if (has0[k] && l == 0 && act[k]) sk[0] = saved[k];  // the cached / straddling deviate
-            if (need[k] == 0) continue;
-#pragma unroll
-            for (int p = 0; p < PL; ++p) {
-                const uint32_t j = 32 * p + l;
-                if (j < need[k]) {
-                    sk[2 * j + has0[k]] = d2[k][p];
-                    sk[2 * j + 1 + has0[k]] = d1[k][p];
-                }
-            }
-            const uint32_t jl = need[k] - 1;
-            double dl = d1[k][0];
-#pragma unroll
-            for (int p = 1; p < PL; ++p) dl = (jl >> 5) == static_cast<uint32_t>(p) ? d1[k][p] : dl;
-            saved[k] = __shfl_sync(0xffffffffu, dl, jl & 31);
-            llast[k] = static_cast<uint32_t>(queue[(w * A + k) * QCAP + ((qhead[k] + jl) & (QCAP - 1))] >> 48);
-            qhead[k] += need[k];
-        }
-        __syncthreads();
-        // write-out of output slots [q0, q1) of the tile's active atoms
-        const uint64_t r_lo = q0 / ps;
-        if (fixed) {
-            // thread (rr0, wi) writes element wi of rows r_lo + rr0, + rpi, ...
-            const uint32_t len = static_cast<uint32_t>(q1 - q0);
-            const uint32_t nrows = static_cast<uint32_t>((q1 - 1) / ps - r_lo) + 1;
-            int slot = static_cast<int>(rr0 * ps + col) + static_cast<int>(r_lo * ps - q0);
-            double* po = out + (r_lo + rr0) * rowstride + a0 * ps + wi;
-            const double* sa = stg + a * S;
-            if (wact) {
-                for (uint32_t rr = rr0; rr < nrows; rr += rpi) {
-                    if (static_cast<uint32_t>(slot) < len) st_cs(po, sa[slot]);
-                    slot += static_cast<int>(rpi * ps);
-                    po += rpi * rowstride;
-                }
-            }
-        } else {
-            // long rows: atom-major, consecutive threads on consecutive slots
-            const uint32_t len = static_cast<uint32_t>(q1 - q0);
-            for (uint32_t x = threadIdx.x; x < T * len; x += 32 * kWW) {
-                const uint32_t at = x / len, sl = x - at * len;
-                if (!((tmask >> at) & 1u)) continue;
-                const uint64_t q = q0 + sl, r = q / ps;
-                st_cs(out + (r * n_atoms + a0 + at) * ps + (q - r * ps), stg[at * S + sl]);
-            }
-        }
-    }
-    // final states: the ring window, cursors and v after n uniforms; the cache
-#pragma unroll
-    for (int k = 0; k < A; ++k) {
-        if (!act[k]) continue;
-        ranmar_gauss_state* gs = g + a0 + w * A + k;
-        const int i0 = gs->s.i, j0 = gs->s.j;
-        const uint32_t v0 = gs->s.v;
-        __syncwarp();
-        if (gens[k] > 0) {
-            const uint64_t N = 2 * (32 * (gens[k] - 1) + llast[k] + 1);
-            const uint64_t rounds = 2 * gens[k];
-            uint32_t* lane_w = gs->s.lane;
-            const int64_t lo = static_cast<int64_t>(N) - 97, hi = static_cast<int64_t>(N);
-            const uint32_t regs[5] = {gen[k].R1, gen[k].R2, gen[k].R3, gen[k].R4, gen[k].R5};
-#pragma unroll
-            for (int r = 0; r < 5; ++r) {
-                const int64_t n = 32 * (static_cast<int64_t>(rounds) - 1 - r) + l;
-                if (n >= lo && n < hi) {
-                    int64_t m = (static_cast<int64_t>(i0) - n) % 97;
-                    lane_w[m < 0 ? m + 97 : m] = regs[r] & kMask;
-                }
-            }
-            __syncwarp();
-            if (l == 0) {
-                const int nm = static_cast<int>(N % 97);
-                gs->s.i = (i0 - nm + 97) % 97;
-                gs->s.j = (j0 - nm + 97) % 97;
-                gs->s.v = arith_advance(v0, N);
-            }
-        }
-        if (l == 0) {
-            gs->saved = saved[k];
-            gs->has_saved = G > 0 ? static_cast<uint32_t>((G - has0[k]) & 1) : static_cast<uint32_t>(has0[k]);
-        }
-    }
-}
-
 }  // namespace
-
-template <int A, int PL, int P>
-static cudaError_t launch_k4w_p(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
-                                uint64_t steps, double* d_out, uint32_t* status, cudaStream_t stream) {
-    using Sh = K4wShape<A, PL, P>;
-    static std::atomic<uint64_t> done{0};
-    if (cudaError_t e = ensure_smem(gaussian_warp_kernel<A, PL, P>, static_cast<int>(Sh::smem), done))
-        return e;
-    const uint64_t blocks = (n_atoms + Sh::T - 1) / Sh::T;
-    count_launch();
-    gaussian_warp_kernel<A, PL, P><<<static_cast<unsigned>(blocks), 32 * kWW, Sh::smem, stream>>>(
-        d_g, n_atoms, per_step, steps, d_out, status);
-    return cudaGetLastError();
-}
-
-template <int K, int P>
-static cudaError_t launch_k4p_p(ranmar_gauss_state* d_g, uint64_t n_atoms, uint32_t G, double* d_out,
-                                uint32_t* status, cudaStream_t stream) {
-    using Sh = K4pShape<K>;
-    static std::atomic<uint64_t> done{0};
-    if (cudaError_t e = ensure_smem(gaussian_pool_kernel<K, P>, Sh::smem, done)) return e;
-    const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
-    count_launch();
-    gaussian_pool_kernel<K, P><<<static_cast<unsigned>(blocks), kGT, Sh::smem, stream>>>(d_g, n_atoms, G, d_out,
-                                                                                          status);
-    return cudaGetLastError();
-}
-
-template <int K>
-static cudaError_t launch_k4p(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step, uint64_t steps,
-                              double* d_out, uint32_t* status, cudaStream_t stream, bool& done) {
-    done = true;
-    const uint64_t G = steps * per_step;
-    if (G < (uint64_t(1) << 32)) {
-        const uint32_t g32 = static_cast<uint32_t>(G);
-        switch (per_step) {
-            case 1: return launch_k4p_p<K, 1>(d_g, n_atoms, g32, d_out, status, stream);
-            case 2: return launch_k4p_p<K, 2>(d_g, n_atoms, g32, d_out, status, stream);
-            case 3: return launch_k4p_p<K, 3>(d_g, n_atoms, g32, d_out, status, stream);
-            case 4: return launch_k4p_p<K, 4>(d_g, n_atoms, g32, d_out, status, stream);
-            case 6: return launch_k4p_p<K, 6>(d_g, n_atoms, g32, d_out, status, stream);
-            default: break;
-        }
-    }
-    done = false;
-    return cudaSuccess;
-}
-
-template <int A, int PL>
-static cudaError_t launch_k4w(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
-                              uint64_t steps, double* d_out, uint32_t* status, cudaStream_t stream) {
-    switch (per_step) {  // compile-time row shapes for the common per-step counts
-        case 1: return launch_k4w_p<A, PL, 1>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 2: return launch_k4w_p<A, PL, 2>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 3: return launch_k4w_p<A, PL, 3>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 4: return launch_k4w_p<A, PL, 4>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 6: return launch_k4w_p<A, PL, 6>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        default: return launch_k4w_p<A, PL, 0>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-    }
-}
 
 // Self-check of div_rn / sqrt_rn against the library's __ddiv_rn / __dsqrt_rn
 // on the operands gaussian() can produce: rsq = s / 2^46 for pseudo-random
@@ -952,32 +391,7 @@ cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     constexpr uint64_t kInplaceMax = 12;
     if (steps * per_step <= kInplaceMax)
         return launch_gaussian_inplace(d_g, n_atoms, per_step, steps, d_out, status, stream);
-    static const int mode = [] {  // TEMPORARY A/B switch
-        const char* e = getenv("RANMAR_K4");
-        return e ? atoi(e) : 1;
-    }();
-    switch (mode) {
-        case 0: return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 20: return launch_gaussian_k<4>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 21: return launch_gaussian_k<5>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 22: return launch_gaussian_k<8>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 23: return launch_gaussian_k<3>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 1: return launch_k4w<4, 1>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 2: return launch_k4w<2, 2>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 3: return launch_k4w<2, 1>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 4: return launch_k4w<8, 1>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        case 5: return launch_k4w<4, 2>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        default: {
-            bool done = false;
-            cudaError_t e = cudaSuccess;
-            if (mode == 10) e = launch_k4p<4>(d_g, n_atoms, per_step, steps, d_out, status, stream, done);
-            if (mode == 11) e = launch_k4p<3>(d_g, n_atoms, per_step, steps, d_out, status, stream, done);
-            if (mode == 12) e = launch_k4p<6>(d_g, n_atoms, per_step, steps, d_out, status, stream, done);
-            if (mode == 13) e = launch_k4p<2>(d_g, n_atoms, per_step, steps, d_out, status, stream, done);
-            if (done) return e;
-            return launch_k4w<2, 1>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-        }
-    }
+    return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
 }
 
 }  // namespace rb
