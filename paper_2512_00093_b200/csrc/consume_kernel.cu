@@ -11,14 +11,18 @@
 // as per_stream calls of step() leave it. No shuffles, no shared-memory
 // traffic for generation: per output one IADD for the lag recurrence, two for
 // v (VIADD + VIADDMNMX), two for the output, half an IADD3 for the sum, and
-// five for the histogram (shift, IMAD address, LOP3 + VIMNMX increment, ATOMS.ADD).
+// four for the histogram (shift, IMAD address, LOP3 increment, ATOMS.ADD).
 //
 // Histogram: thread-private counters in shared memory, thread t owning bank
 // t mod 32: the 32-bit word (bin >> 1) * kCT + t holds bin 2w in its low half
 // and bin 2w + 1 in its high half. One output is ONE shared-memory reduction
 // (red.shared.add, conflict-free since every lane hits its own bank) adding
-// inc = max(u & 2^16, 1), i.e. 1 or 2^16 (measured 4 % faster than the
-// equivalent (u & 2^16) | 1 with a subtraction at flush time). A thread
+// inc = (u & 2^16) | 1, one LOP3 (written as inline lop3: the compiler splits the
+// C expression into an AND and an OR): the low half counts every output of
+// the word's two bins, the high half the odd bin's, and the flush takes
+// lo - hi. Config 4: 410 ms with inc = max(u & 2^16, 1) (LOP3 + VIMNMX, both
+// ALU-pipe, the pipe ncu shows 87 % busy), 369 ms with the single LOP3; moving
+// the u >> 17 shift to an IMAD.HI made it 437 ms. A thread
 // flushes its counters into its stream's u32 histogram in HBM at least every
 // 65,475 outputs, so the low half never carries into the high one.
 #include <cstdint>
@@ -46,7 +50,8 @@ __device__ __forceinline__ void flush(uint32_t* col, uint32_t* __restrict__ gh, 
 #pragma unroll 4
     for (int w = 0; w < kRows; ++w) {
         const uint32_t x = col[w * kCT];
-        const uint32_t hi = x >> 16, lo = x & 0xFFFFu;
+        // every output of the word's two bins added 1 to the low half
+        const uint32_t hi = x >> 16, lo = (x & 0xFFFFu) - hi;
         if (accumulate) {
             gh[2 * w] += lo;
             gh[2 * w + 1] += hi;
@@ -61,7 +66,9 @@ __device__ __forceinline__ void flush(uint32_t* col, uint32_t* __restrict__ gh, 
 // One output's histogram update: a single shared-memory reduction.
 __device__ __forceinline__ void hist_add(uint32_t hb, uint32_t u) {
     const uint32_t a = hb + (u >> 17) * (4 * kCT);
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(max(u & 0x10000u, 1u)) : "memory");
+    uint32_t inc;  // (u & 2^16) | 1 as ONE lop3
+    asm("lop3.b32 %0, %1, 65536, %2, 0xEA;" : "=r"(inc) : "r"(u), "r"(1u));
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(inc) : "memory");
 }
 
 template <int S>
