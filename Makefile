@@ -8,7 +8,7 @@ PKG := paper_2512_00093_b200
 CSRC := $(PKG)/csrc
 BUILD := $(PKG)/build
 LIB := $(PKG)/lib/libranmar_b200.so
-OBJS := $(BUILD)/gen_kernels.o $(BUILD)/float_kernel.o $(BUILD)/consume_kernel.o $(BUILD)/gauss_kernel.o $(BUILD)/gauss_reg_kernel.o $(BUILD)/gauss_stream_kernel.o $(BUILD)/langevin_kernel.o $(BUILD)/jump_kernels.o $(BUILD)/text_kernels.o $(BUILD)/ranmar_abi.o
+OBJS := $(BUILD)/gen_kernels.o $(BUILD)/float_kernel.o $(BUILD)/consume_kernel.o $(BUILD)/gauss_kernel.o $(BUILD)/gauss_stream_kernel.o $(BUILD)/langevin_kernel.o $(BUILD)/jump_kernels.o $(BUILD)/text_kernels.o $(BUILD)/ranmar_abi.o
 HDRS := include/ranmar_b200.h $(CSRC)/ranmar_device.cuh $(CSRC)/gauss_math.cuh $(CSRC)/crlog_table.inc
 
 .PHONY: all lib oracle ref clean sass

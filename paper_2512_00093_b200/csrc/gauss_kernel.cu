@@ -24,7 +24,6 @@
 // whatever the (diverged) cursors. States are moved between HBM and the ring
 // with 16-B vector accesses (the 416-B records are 16-B aligned).
 #include <cstdint>
-#include <cstdlib>
 #include <type_traits>
 
 #include "gauss_math.cuh"
@@ -381,8 +380,6 @@ cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_
 
 cudaError_t launch_gaussian_inplace(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*,
                                     uint32_t*, cudaStream_t);
-cudaError_t launch_gaussian_reg(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
-                                cudaStream_t);
 
 cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, uint32_t* status,
@@ -394,9 +391,7 @@ cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     constexpr uint64_t kInplaceMax = 12;
     if (steps * per_step <= kInplaceMax)
         return launch_gaussian_inplace(d_g, n_atoms, per_step, steps, d_out, status, stream);
-    static const bool old = getenv("RANMAR_K4OLD") != nullptr;  // TEMPORARY A/B switch
-    if (old) return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
-    return launch_gaussian_reg(d_g, n_atoms, per_step, steps, d_out, status, stream);
+    return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
 }
 
 }  // namespace rb
