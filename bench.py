@@ -636,18 +636,26 @@ def run_ours(args, rank, world, local):
         del st5, ws5
         out5 = torch.empty((C5["steps"], n5, C5["per"]), dtype=torch.float64, device=dev)
         g5w = g5.clone()
-        rb.gaussian(g5w, C5["per"], 2, out=out5[:2], stream=stream)  # warm-up
-        torch.cuda.synchronize()
-        g5w.copy_(g5)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        # warm-up: the full launch (the kernel K4 runs; a short launch would take the
+        # in-place K6 path and leave K4's first-launch module load in the timed region)
         rb.gaussian(g5w, C5["per"], C5["steps"], out=out5, stream=stream)
-        b.record(stream)
         torch.cuda.synchronize()
-        ms5 = max_over_ranks(a.elapsed_time(b), world)
+        trials5 = []
+        for _ in range(3):  # each trial from the same start states, copied outside the timing
+            g5w.copy_(g5)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rb.gaussian(g5w, C5["per"], C5["steps"], out=out5, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            trials5.append(max_over_ranks(a.elapsed_time(b), world))
+        ms5 = sorted(trials5)[1]
         nbytes = out5.numel() * 8 + 2 * n5 * 416
         extras["config5"] = {"workload": "2^24 atoms x 3 gaussian() x 100 steps per rank, fp64 out",
                              "gaussians_per_s": out5.numel() * world / (ms5 * 1e-3), "ms": ms5,
+                             "timing": "median of 3 launches after a full warm-up launch",
+                             "ms_trials": trials5,
                              "GB_per_s": nbytes / (ms5 * 1e-3) / 1e9,
                              "roofline": {"bound": "hbm", "unit": "GB/s",
                                           "achieved": nbytes / (ms5 * 1e-3) / 1e9, "peak": peak,
