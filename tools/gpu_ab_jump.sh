@@ -1,0 +1,6 @@
+# A/B of jump_kernels.cu variants: each variant file is copied in, rebuilt, checked and timed.
+for v in "$@"; do
+  cp $v paper_2512_00093_b200/csrc/jump_kernels.cu && make lib > /dev/null 2>&1 && echo "variant $v" && \
+  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "make_streams or three_level or config3 or jump" 2>&1 | tail -1 && \
+  python tools/time_c3.py --reps 50 | tail -1
+done
