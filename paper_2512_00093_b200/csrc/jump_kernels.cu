@@ -332,6 +332,9 @@ __device__ __forceinline__ void extend_items(uint32_t* W, int stride, int items,
 // Level kernels process kApplyItems states per CTA (shared-memory Hankel tiles):
 // 8, or 1 for small levels (a tree's top levels: 64 states would be 8 CTAs).
 constexpr int kApplyItemsMax = 8;
+#ifndef RB_LEVEL_JS
+#define RB_LEVEL_JS 4
+#endif
 constexpr int kJPad = 104;                        // coefficients padded to 13 x 8
 
 // ---- K3b/K3c for a batch, tiled: out[k] = jump(in[k]) with one shared P.
@@ -459,19 +462,23 @@ __global__ void __launch_bounds__(kA2Threads, 3)
 // instead of a decanonicalized state.
 constexpr int kWAnchor = 196;  // words per anchor extension row (193 used)
 
-template <bool WMODE, int kApplyItems>
-__global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13))
+// JS > 1 (one state per CTA, the tree's small top levels, where latency is all
+// that matters): the 13 j-chunks of 8 are split over JS thread groups and the
+// partial columns summed through shared memory.
+template <bool WMODE, int kApplyItems, int JS = 1>
+__global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13) * JS)
     level_kernel(const ranmar_state* __restrict__ in, uint64_t count,
                  const uint32_t* __restrict__ Tab, uint32_t c_lvl, ranmar_state* __restrict__ out,
                  uint32_t* __restrict__ outW, uint32_t* __restrict__ outV) {
     constexpr int CG = WMODE ? 25 : 13;          // column groups of 8
-    constexpr int NT = kApplyItems * CG;
+    constexpr int NT = kApplyItems * CG * JS;
     constexpr int EXT = 97 + 8 * CG;             // 297 / 201
     constexpr int STR = (EXT + 8) | 1;           // odd stride
     __shared__ uint32_t W[kApplyItems * STR];
     __shared__ uint32_t p[kApplyItems][kJPad];
     __shared__ uint32_t vin[kApplyItems];
     __shared__ int iin[kApplyItems];
+    __shared__ uint32_t part[JS > 1 ? kApplyItems * (JS - 1) * 8 * CG : 1];
     const int t = threadIdx.x;
     const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kApplyItems;
     const int items = static_cast<int>(count - k0 < (uint64_t)kApplyItems ? count - k0 : (uint64_t)kApplyItems);
@@ -492,26 +499,43 @@ __global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13))
     __syncthreads();
     extend_items(W, STR, items, EXT + 8, t, NT);
 
-    const int it = t / CG, cg = t - it * CG;
-    if (it >= items) return;
-    const uint32_t* w_it = W + it * STR + 8 * cg;
-    const uint32_t* p_it = p[it];
-    uint32_t acc[8], win[8];
+    const int it = t / (CG * JS), rem = t - it * (CG * JS);
+    const int cg = rem % CG, js = rem / CG;
+    const bool live = it < items;
+    uint32_t acc[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        acc[c] = 0;
-        win[c] = w_it[c];
-    }
+    for (int c = 0; c < 8; ++c) acc[c] = 0;
+    if (live) {
+        const uint32_t* w_it = W + it * STR + 8 * cg;
+        const uint32_t* p_it = p[it];
+        uint32_t win[8];
 #pragma unroll 1
-    for (int j0 = 0; j0 < kJPad; j0 += 8) {
+        for (int q = js; q < kJPad / 8; q += JS) {
+            const int j0 = 8 * q;
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-            const uint32_t pj = p_it[j0 + jj];
+            for (int c = 0; c < 8; ++c) win[c] = w_it[j0 + c];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[c] += pj * win[(jj + c) & 7];
-            win[jj] = w_it[j0 + jj + 8];
+            for (int jj = 0; jj < 8; ++jj) {
+                const uint32_t pj = p_it[j0 + jj];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[c] += pj * win[(jj + c) & 7];
+                win[jj] = w_it[j0 + jj + 8];
+            }
         }
     }
+    if (JS > 1) {
+        if (live && js > 0) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) part[((it * (JS - 1) + js - 1) * CG + cg) * 8 + c] = acc[c];
+        }
+        __syncthreads();
+        if (!live || js > 0) return;
+#pragma unroll
+        for (int s2 = 0; s2 < JS - 1; ++s2)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] += part[((it * (JS - 1) + s2) * CG + cg) * 8 + c];
+    }
+    if (!live) return;
     const uint64_t k = k0 + it;
     const uint64_t r = k % kRows;
     const uint32_t dec = static_cast<uint32_t>((r * c_lvl % kMod) * kDelta % kMod);
@@ -1540,11 +1564,12 @@ cudaError_t launch_level(const ranmar_state* in, uint64_t count, const uint32_t*
                          cudaStream_t stream) {
     count_launch();
     if (count <= 1024) {  // one state per CTA: the level's latency, not its MACs, matters
+        constexpr int JS = RB_LEVEL_JS;  // j-chunks split over JS thread groups
         const unsigned blocks = static_cast<unsigned>(count);
         if (outW)
-            level_kernel<true, 1><<<blocks, 25, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
+            level_kernel<true, 1, JS><<<blocks, 25 * JS, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
         else
-            level_kernel<false, 1><<<blocks, 13, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
+            level_kernel<false, 1, JS><<<blocks, 13 * JS, 0, stream>>>(in, count, Tab, c_lvl, out, outW, outV);
         return cudaGetLastError();
     }
     constexpr int I = kApplyItemsMax;
