@@ -612,7 +612,7 @@ def run_ours(args, rank, world, local):
             extras["config4"]["roofline"] = {
                 "bound": "int_issue", "unit": "Tops/s", "achieved": ach / 1e12,
                 "peak": ip["int_issue"] / 1e12, "frac": ach / ip["int_issue"],
-                "peak_kind": f"measured ({ip['source']}, best IADD3/IMAD mix)",
+                "peak_kind": f"measured ({ip['source']}, best of the IADD3, IADD3+IMAD and IADD3+IMAD+LOP3 issue rates)",
                 "algorithmic_per_unit": "9 int32 ops per uniform (SURVEY §8d C4)"}
         # after timing: all-gather the per-stream sums, all-reduce the histogram
         from paper_2512_00093_b200.shard import allgather_tensor, allreduce_sum
