@@ -660,6 +660,27 @@ def run_ours(args, rank, world, local):
                              "roofline": {"bound": "hbm", "unit": "GB/s",
                                           "achieved": nbytes / (ms5 * 1e-3) / 1e9, "peak": peak,
                                           "frac": nbytes / (ms5 * 1e-3) / 1e9 / peak}}
+        # the same deviates consumed in-kernel (§8f row 4): per-atom sum and sum of
+        # squares, nothing stored -- the gaussian() rate without the store
+        mom5 = torch.empty((n5, 2), dtype=torch.float64, device=dev)
+        g5w.copy_(g5)
+        rb.gaussian_moments(g5w, C5["per"] * C5["steps"], out=mom5, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        trials_m = []
+        for _ in range(3):
+            g5w.copy_(g5)
+            torch.cuda.synchronize()
+            a.record(stream)
+            rb.gaussian_moments(g5w, C5["per"] * C5["steps"], out=mom5, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            trials_m.append(max_over_ranks(a.elapsed_time(b), world))
+        ms_m = sorted(trials_m)[1]
+        extras["config5_moments"] = {
+            "workload": "config 5's deviates consumed in-kernel: per-atom sum and sum of squares, no store",
+            "ms": ms_m, "ms_trials": trials_m,
+            "gaussians_per_s": n5 * C5["per"] * C5["steps"] * world / (ms_m * 1e-3)}
+        del mom5
         # after timing: every rank's deviate sum and sum of squares, all-gathered
         from paper_2512_00093_b200.shard import allgather_tensor
         mom = torch.stack([out5.sum(dtype=torch.float64), (out5 * out5).sum(dtype=torch.float64)])

@@ -182,6 +182,15 @@ int ranmar_consume_dev(ranmar_state* d_states, uint64_t n_streams, uint64_t per_
 int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t per_step,
                             uint64_t steps, double* d_out, void* stream);
 
+/* gaussian() consumed in-kernel (no reference counterpart):
+ * for each atom, count gaussian() calls (the cached deviate first, as
+ * ranmar_gaussian_f64_dev with per_step = count, steps = 1) summed in call
+ * order, d_out[2 atom] = s1, d_out[2 atom + 1] = s2 with s1 = RN(s1 + x),
+ * s2 = RN(s2 + RN(x * x)); nothing else is stored. States and caches advance
+ * exactly as that ranmar_gaussian_f64_dev call would leave them. */
+int ranmar_gaussian_moments_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t count, double* d_out,
+                                void* stream);
+
 /* Fix-langevin-style per-atom consumer (no reference counterpart; SURVEY
  * §8f rows 3-4): one stream per atom, uniforms/gaussians consumed in-kernel.
  * For each atom a with d_mask == NULL or (d_mask[a] & groupbit) != 0, with

@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         "ranmar_generate_f64_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_consume_dev": (i32, [vp, u64, u64, vp, vp, vp]),
         "ranmar_gaussian_f64_dev": (i32, [vp, u64, u64, u64, vp, vp]),
+        "ranmar_gaussian_moments_dev": (i32, [vp, u64, u64, vp, vp]),
         "ranmar_fp64_selfcheck_dev": (i32, [u64, u64, vp, vp]),
         "ranmar_crlog_sweep_dev": (i32, [u64, u64, i32, vp, vp, u64, vp]),
         "ranmar_bank_words": (u64, [u64]),
@@ -400,6 +401,21 @@ def gaussian(gstates, per_step: int, steps: int, out=None, stream=None):
         out = torch.empty((steps, n, per_step), dtype=torch.float64, device="cuda")
     _check(lib().ranmar_gaussian_f64_dev(_dptr(gstates), n, per_step, steps, _dptr(out),
                                          _stream_ptr(stream)))
+    return out
+
+
+@_on_device
+def gaussian_moments(gstates, count: int, out=None, stream=None):
+    """count gaussian() calls per atom consumed in-kernel -> out[atom] = (sum, sum of
+    squares) in call order (float64 [n, 2]); states advance as gaussian(g, count, 1)."""
+    torch = _torch()
+    n = gstates.shape[0]
+    if out is None:
+        out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    if count == 0:
+        out.zero_()
+        return out
+    _check(lib().ranmar_gaussian_moments_dev(_dptr(gstates), n, count, _dptr(out), _stream_ptr(stream)))
     return out
 
 

@@ -65,6 +65,10 @@ __device__ __forceinline__ void ring_st(uint32_t off, uint32_t x) {
 // 2K / P whole rows of the output, so its 2K stores address row pointers with
 // immediate column offsets instead of walking the (row, column) countdown per
 // deviate (~6.5 instructions each, ncu source page).
+// P == -1: the moments consumer (ranmar_gaussian_moments_dev, §8f row 4): no
+// deviate is stored; each atom's steps * per_step deviates (its cached one
+// first) are summed in order, s1 = RN(s1 + x), s2 = RN(s2 + RN(x * x)), and
+// out[2 atom], out[2 atom + 1] = s1, s2.
 template <int K, int P>
 __global__ void __launch_bounds__(kGT)
     gaussian_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
@@ -115,7 +119,13 @@ __global__ void __launch_bounds__(kGT)
     const uint64_t jump = (n_atoms - 1) * per_step;
     const uint32_t row = per_step < 0xFFFFFFFFull ? static_cast<uint32_t>(per_step) : 0xFFFFFFFFu;
     uint32_t left = row;
+    double s1 = 0.0, s2 = 0.0;  // P == -1
     auto put = [&](double x) {
+        if (P < 0) {
+            s1 = __dadd_rn(s1, x);
+            s2 = __dadd_rn(s2, __dmul_rn(x, x));
+            return;
+        }
         st_cs(po, x);
         ++po;
         if (--left == 0) {
@@ -268,6 +278,10 @@ __global__ void __launch_bounds__(kGT)
                    static_cast<uint32_t>(i >= 64 ? i - 64 : i + 33), v);
     gs->saved = saved;
     gs->has_saved = has ? 1u : 0u;
+    if (P < 0) {
+        out[2 * atom] = s1;
+        out[2 * atom + 1] = s2;
+    }
 }
 
 }  // namespace
@@ -375,6 +389,17 @@ cudaError_t launch_gaussian_k(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_
         case 6: go(std::integral_constant<int, 6>{}); break;
         default: go(std::integral_constant<int, 0>{});
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gaussian_moments(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t count,
+                                    double* d_out, uint32_t* status, cudaStream_t stream) {
+    if (n_atoms == 0 || count == 0) return cudaSuccess;
+    const int smem = 97 * kGT * 4;
+    const uint64_t blocks = (n_atoms + kGT - 1) / kGT;
+    count_launch();
+    gaussian_kernel<kBatch, -1><<<static_cast<unsigned>(blocks), kGT, smem, stream>>>(d_g, n_atoms, count, 1,
+                                                                                      d_out, status);
     return cudaGetLastError();
 }
 

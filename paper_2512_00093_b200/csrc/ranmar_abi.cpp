@@ -46,6 +46,7 @@ cudaError_t launch_to_text(const ranmar_state*, uint64_t, char*, uint64_t*, void
                            cudaStream_t);
 cudaError_t launch_from_text(const char*, const uint64_t*, uint64_t, ranmar_state*, int32_t*,
                              cudaStream_t);
+cudaError_t launch_gaussian_moments(ranmar_gauss_state*, uint64_t, uint64_t, double*, uint32_t*, cudaStream_t);
 cudaError_t launch_gaussian(ranmar_gauss_state*, uint64_t, uint64_t, uint64_t, double*, uint32_t*,
                             cudaStream_t);
 cudaError_t launch_langevin(ranmar_gauss_state*, uint64_t, const double*, double*, const int32_t*,
@@ -802,6 +803,15 @@ int ranmar_gaussian_f64_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     RB_CUDA(rb::launch_gaussian(d_g, n_atoms, per_step, steps, d_out, status,
                                 static_cast<cudaStream_t>(stream)),
             "gaussian_kernel launch");
+    return RANMAR_OK;
+}
+
+int ranmar_gaussian_moments_dev(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t count, double* d_out,
+                                void* stream) {
+    if (n_atoms && count && (!d_g || !d_out)) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_gaussian_moments(d_g, n_atoms, count, d_out, status, static_cast<cudaStream_t>(stream)),
+            "gaussian_kernel (moments) launch");
     return RANMAR_OK;
 }
 

@@ -121,6 +121,7 @@ def test_device_entry_points_validate_arguments_first():
     assert lib.ranmar_generate_f32_dev(vp, 4, 4, None, None) == EINVAL
     assert lib.ranmar_consume_dev(vp, 4, 4, None, vp, None) == EINVAL
     assert lib.ranmar_gaussian_f64_dev(None, 4, 3, 2, vp, None) == EINVAL
+    assert lib.ranmar_gaussian_moments_dev(vp, 4, 3, None, None) == EINVAL
     assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, 1, 1.0, 7, None) == EINVAL
     assert lib.ranmar_langevin_dev(vp, 4, vp, vp, vp, None, 1, vp, vp, -1, 1.0, 0, None) == EINVAL
     assert lib.ranmar_langevin_dev(vp, 4, None, vp, vp, None, 1, vp, vp, 1, 1.0, 0, None) == EINVAL

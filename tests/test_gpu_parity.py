@@ -362,6 +362,29 @@ def test_gaussian_odd_count_keeps_cache(oracle):
     assert gh.tobytes() == og.tobytes()  # states, cursors, cached deviate
 
 
+@pytest.mark.parametrize("count", [1, 2, 13, 300, 1001])
+def test_gaussian_moments_consumer(oracle, count):
+    # §8f row 4: gaussian() consumed in-kernel (K4 without stores): per atom the
+    # sum and sum of squares of its `count` deviates in call order (cached one
+    # first), bit-exact against sequential sums of the oracle's deviates; states
+    # and caches advance exactly as a gaussian() call of the same length
+    from oracle.bind import GAUSS_DTYPE
+    n = 70
+    og = np.zeros(n, GAUSS_DTYPE)
+    og["s"] = random_states(n, 9100 + count, oracle)
+    og["has_saved"][::4] = 1
+    og["saved"][::4] = np.linspace(-1.5, 1.5, len(og[::4]))
+    g = torch.from_numpy(og.copy().view(np.int32).reshape(n, rb.GAUSS_WORDS)).cuda()
+    mom = rb.gaussian_moments(g, count).cpu().numpy()
+    exp = oracle.gaussian_fill(og, count, 1).reshape(n, count)
+    s1 = np.cumsum(exp, axis=1)[:, -1]
+    s2 = np.cumsum(exp * exp, axis=1)[:, -1]
+    assert mom[:, 0].tobytes() == s1.tobytes() and mom[:, 1].tobytes() == s2.tobytes()
+    gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
+    assert gh.tobytes() == og.tobytes()
+    assert rb.device_status(clear=True) == 0
+
+
 @pytest.mark.parametrize("per_step,steps", [(1, 1), (2, 3), (3, 100), (7, 40), (300, 2), (257, 1),
                                             (5, 77)])
 def test_gaussian_shapes(oracle, per_step, steps):

@@ -20,17 +20,23 @@ def main():
     ap.add_argument("--per", type=int, default=3)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--moments", action="store_true", help="time the in-kernel moments consumer instead")
     a = ap.parse_args()
     g = rb.gauss_states_from(rb.make_streams(7, 2**50, a.atoms))
-    out = torch.empty((a.steps, a.atoms, a.per), dtype=torch.float64, device="cuda")
+    if a.moments:
+        out = torch.empty((a.atoms, 2), dtype=torch.float64, device="cuda")
+        run = lambda: rb.gaussian_moments(g, a.per * a.steps, out=out)  # noqa: E731
+    else:
+        out = torch.empty((a.steps, a.atoms, a.per), dtype=torch.float64, device="cuda")
+        run = lambda: rb.gaussian(g, a.per, a.steps, out=out)  # noqa: E731
     for _ in range(2):
-        rb.gaussian(g, a.per, a.steps, out=out)
+        run()
     ts = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
-        rb.gaussian(g, a.per, a.steps, out=out)
+        run()
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -38,7 +44,7 @@ def main():
     ms = sorted(ts)[len(ts) // 2]
     dev = a.atoms * a.per * a.steps
     by = dev * 8 + a.atoms * 2 * 416
-    print(f"k4 atoms={a.atoms} per={a.per} steps={a.steps}: median {ms:.3f} ms (all {[round(t, 3) for t in ts]}), "
+    print(f"k4{' moments' if a.moments else ''} atoms={a.atoms} per={a.per} steps={a.steps}: median {ms:.3f} ms (all {[round(t, 3) for t in ts]}), "
           f"{dev / ms / 1e6:.3e} gaussians/s, {by / ms / 1e6:.1f} GB/s")
 
 
