@@ -24,7 +24,6 @@
 // whatever the (diverged) cursors. States are moved between HBM and the ring
 // with 16-B vector accesses (the 416-B records are 16-B aligned).
 #include <cstdint>
-#include <cstdlib>
 #include <type_traits>
 
 #include "gauss_math.cuh"
@@ -285,210 +284,6 @@ __global__ void __launch_bounds__(kGT)
     }
 }
 
-// ---------------------------------------------------------------- K4x2
-// Two lanes per atom (EXPERIMENT): lane h of atom a computes the uniforms
-// 2m + h of each attempt m on the atom's shared-memory ring (cursors stepped by
-// two), the pair is exchanged with one shuffle, and each lane evaluates the
-// fp64 chains of every other accepted pair (K/2 each). Same shared memory per
-// atom as K4, twice the threads.
-#ifndef RB_K4X2_MINB
-#define RB_K4X2_MINB 6
-#endif
-constexpr int kG2 = 64;  // atoms per block (2 kG2 threads)
-constexpr uint32_t kStep2A = static_cast<uint32_t>((2ull * kStepA) % kMod);
-
-template <int K, int P>
-__global__ void __launch_bounds__(2 * kG2, RB_K4X2_MINB)
-    gaussian2_kernel(ranmar_gauss_state* __restrict__ g, uint64_t n_atoms, uint64_t per_step,
-                     uint64_t steps, double* __restrict__ out, uint32_t* status) {
-    static_assert(K % 2 == 0, "pairs alternate between the two lanes");
-    constexpr int KH = K / 2;
-    extern __shared__ uint32_t ring[];  // [97][kG2]
-    const int t = threadIdx.x, h = t & 1, a = t >> 1;
-    if (static_cast<uint32_t>(__cvta_generic_to_shared(ring)) != kRingBase) {
-        if (t == 0) atomicOr(status, kStatusInternal);
-        return;
-    }
-    const uint64_t atom = static_cast<uint64_t>(blockIdx.x) * kG2 + a;
-    if (atom >= n_atoms) return;
-    ranmar_gauss_state* gs = g + atom;
-    const int i0 = gs->s.i, j0 = gs->s.j;
-    const uint32_t v0 = gs->s.v;
-    if (!state_ok(i0, j0, v0)) {
-        if (h == 0) atomicOr(status, kStatusBadState);
-        return;
-    }
-    {   // lanes -> ring column a: 16-B chunks split between the pair
-        const uint4* src = reinterpret_cast<const uint4*>(gs->s.lane);
-#pragma unroll 4
-        for (int qq = 0; qq < 12; ++qq) {
-            const int c = 2 * qq + h;
-            const uint4 x = src[c];
-            ring[(4 * c + 0) * kG2 + a] = x.x;
-            ring[(4 * c + 1) * kG2 + a] = x.y;
-            ring[(4 * c + 2) * kG2 + a] = x.z;
-            ring[(4 * c + 3) * kG2 + a] = x.w;
-        }
-        if (h == 0) ring[96 * kG2 + a] = gs->s.lane[96];
-    }
-    __syncwarp(__activemask());
-    constexpr uint32_t kSlot = 4 * kG2;
-    const uint32_t base = 4 * a;
-    int si = i0 - h;
-    si += si < 0 ? 97 : 0;
-    int sj = si + 33;
-    sj -= sj >= 97 ? 97 : 0;
-    uint32_t ai = base + si * kSlot, aj = base + sj * kSlot;
-    // two slots down with wraparound: slot s >= 2 -> s - 2, s < 2 -> s + 95
-    auto dec2 = [&](uint32_t x) { return min(x - 2 * kSlot, x + 95 * kSlot); };
-    uint32_t v = arith_advance(v0, static_cast<uint64_t>(h) + 1);  // v of this lane's next uniform
-    double saved = gs->saved;
-    bool has = gs->has_saved != 0;
-
-    const uint64_t G = steps * per_step;
-    uint64_t q = 0;
-    double* po = out + atom * per_step;
-    const uint64_t jump = (n_atoms - 1) * per_step;
-    const uint32_t row = per_step < 0xFFFFFFFFull ? static_cast<uint32_t>(per_step) : 0xFFFFFFFFu;
-    uint32_t left = row;
-    // both lanes walk the output position; lane 0 stores
-    auto put = [&](double x) {
-        if (h == 0) st_cs(po, x);
-        ++po;
-        if (--left == 0) {
-            left = row;
-            po += jump;
-        }
-    };
-    if (has && G > 0) {
-        put(saved);
-        has = false;
-        q = 1;
-    }
-    uint32_t c0 = ring_ld(ai), c1 = ring_ld(aj);
-    auto attempt = [&](uint32_t& u0, uint32_t& u1) -> bool {
-        const uint32_t a2 = dec2(ai), j2 = dec2(aj);
-        const uint32_t x = c0 - c1;
-        c0 = ring_ld(a2);
-        c1 = ring_ld(j2);
-        ring_st(ai, x);
-        ai = a2;
-        aj = j2;
-        const uint32_t u = (x - v) & kMask;
-        v = add_mod_m(v, kStep2A);
-        const uint32_t uo = __shfl_xor_sync(__activemask(), u, 1);
-        u0 = h ? uo : u;
-        u1 = h ? u : uo;
-        const int32_t da = static_cast<int32_t>(u0) - (1 << 23);
-        const int32_t db = static_cast<int32_t>(u1) - (1 << 23);
-        const int64_t s = static_cast<int64_t>(da) * da + static_cast<int64_t>(db) * db;
-        return s > 0 && s < (int64_t(1) << 46);
-    };
-    static_assert(P == 0 || (2 * K) % P == 0, "whole rows per batch");
-    const bool rows_fast = P > 0 && __all_sync(__activemask(), q == 0);
-    const uint64_t row_stride = n_atoms * per_step;
-    while (G - q >= 2 * K) {
-        uint32_t ah[KH], bh[KH];
-        for (int got = 0; got < K;) {
-            uint32_t u0, u1;
-            if (attempt(u0, u1)) {
-                if ((got & 1) == h) {
-#pragma unroll
-                    for (int k = 0; k + 1 < KH; ++k) {
-                        ah[k] = ah[k + 1];
-                        bh[k] = bh[k + 1];
-                    }
-                    ah[KH - 1] = u0;
-                    bh[KH - 1] = u1;
-                }
-                ++got;
-            }
-        }
-        double d1[KH], d2[KH];
-        {
-            double rsq[KH], lg[KH];
-            bool all_ok = true;
-#pragma unroll
-            for (int k = 0; k < KH; ++k) {
-                rsq[k] = polar_rsq(ah[k], bh[k]);
-                bool ok;
-                lg[k] = crlog_fast(rsq[k], ok);
-                all_ok = all_ok && ok;
-            }
-            if (__builtin_expect(!all_ok, 0)) {
-#pragma unroll
-                for (int k = 0; k < KH; ++k) {
-                    bool ok;
-                    crlog_fast(rsq[k], ok);
-                    if (!ok) lg[k] = crlog_accurate(rsq[k]).y;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < KH; ++k) {
-                const double fac = polar_fac_of(rsq[k], lg[k]);
-                d2[k] = __dmul_rn(polar_v(bh[k]), fac);
-                d1[k] = __dmul_rn(polar_v(ah[k]), fac);
-            }
-        }
-        const unsigned mask = __activemask();
-        if (P > 0 && rows_fast) {  // po at the start of a row; lane h holds pairs 2j + h
-            constexpr int PP = P > 0 ? P : 1;
-#pragma unroll
-            for (int k = 0; k < KH; ++k) {
-                const uint32_t p0 = 4 * k + 2 * h;  // batch positions p0, p0 + 1
-                const uint32_t r0 = p0 / PP, c0p = p0 - r0 * PP;
-                const uint32_t r1 = (p0 + 1) / PP, c1p = (p0 + 1) - r1 * PP;
-                st_cs(po + r0 * row_stride + c0p, d2[k]);
-                st_cs(po + r1 * row_stride + c1p, d1[k]);
-            }
-            po += (2 * K / PP) * row_stride;
-        } else {  // in call order through lane 0
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int src = (threadIdx.x & 31 & ~1) | (k & 1);
-                const double x2 = __shfl_sync(mask, d2[k >> 1], src);
-                const double x1 = __shfl_sync(mask, d1[k >> 1], src);
-                put(x2);
-                put(x1);
-            }
-        }
-        saved = __shfl_sync(mask, d1[KH - 1], (threadIdx.x & 31) | 1);  // pair K - 1: lane 1's last chain
-        q += 2 * K;
-    }
-    while (q < G) {
-        uint32_t u0, u1;
-        while (!attempt(u0, u1)) {
-        }
-        const double fac = polar_fac(u0, u1);
-        saved = __dmul_rn(polar_v(u0), fac);
-        put(__dmul_rn(polar_v(u1), fac));
-        if (q + 1 < G) {
-            put(saved);
-        } else {
-            has = true;
-        }
-        q += 2;
-    }
-    __syncwarp(__activemask());
-    {   // ring -> lanes, chunks split between the pair; lane 0 the record tail
-        uint4* dst = reinterpret_cast<uint4*>(gs->s.lane);
-#pragma unroll 4
-        for (int qq = 0; qq < 12; ++qq) {
-            const int c = 2 * qq + h;
-            dst[c] = make_uint4(ring[(4 * c + 0) * kG2 + a] & kMask, ring[(4 * c + 1) * kG2 + a] & kMask,
-                                ring[(4 * c + 2) * kG2 + a] & kMask, ring[(4 * c + 3) * kG2 + a] & kMask);
-        }
-    }
-    if (h == 0) {
-        const int i = static_cast<int>((ai - base) / kSlot);  // slot of the next uniform
-        *reinterpret_cast<uint4*>(gs->s.lane + 96) =
-            make_uint4(ring[96 * kG2 + a] & kMask, static_cast<uint32_t>(i),
-                       static_cast<uint32_t>(i >= 64 ? i - 64 : i + 33), add_mod_m(v, kDelta));
-        gs->saved = saved;
-        gs->has_saved = has ? 1u : 0u;
-    }
-}
-
 }  // namespace
 
 // Self-check of div_rn / sqrt_rn against the library's __ddiv_rn / __dsqrt_rn
@@ -621,21 +416,6 @@ cudaError_t launch_gaussian(ranmar_gauss_state* d_g, uint64_t n_atoms, uint64_t 
     constexpr uint64_t kInplaceMax = 12;
     if (steps * per_step <= kInplaceMax)
         return launch_gaussian_inplace(d_g, n_atoms, per_step, steps, d_out, status, stream);
-    static const bool x2 = getenv("RB_K4X2") != nullptr;  // TEMPORARY A/B switch
-    if (x2) {
-        const int smem = 97 * kG2 * 4;
-        const dim3 grid(static_cast<unsigned>((n_atoms + kG2 - 1) / kG2));
-        count_launch();
-        switch (per_step) {
-            case 1: gaussian2_kernel<6, 1><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
-            case 2: gaussian2_kernel<6, 2><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
-            case 3: gaussian2_kernel<6, 3><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
-            case 4: gaussian2_kernel<6, 4><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
-            case 6: gaussian2_kernel<6, 6><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status); break;
-            default: gaussian2_kernel<6, 0><<<grid, 2 * kG2, smem, stream>>>(d_g, n_atoms, per_step, steps, d_out, status);
-        }
-        return cudaGetLastError();
-    }
     return launch_gaussian_k<kBatch>(d_g, n_atoms, per_step, steps, d_out, status, stream);
 }
 
