@@ -158,39 +158,90 @@ __global__ void __launch_bounds__(256)
 // an in-place AoS update touches.
 constexpr int kBankRows = 99;
 
-__global__ void bank_from_states_kernel(const ranmar_state* __restrict__ st, uint64_t n,
-                                        uint32_t* __restrict__ bank, uint32_t* status) {
-    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n) return;
-    const ranmar_state* r = st + a;
-    const int i0 = r->i;
-    if (!state_ok(i0, r->j, r->v)) atomicOr(status, kStatusBadState);
-    const int ic = static_cast<unsigned>(i0) < 97u ? i0 : 0;
-#pragma unroll 4
-    for (int s = 0; s < 97; ++s) {
-        const int q = ic - s;
-        bank[s * n + a] = r->lane[q < 0 ? q + 97 : q];
+// AoS records <-> slot-major bank, tiled: a block moves 64 records through a
+// shared-memory tile [slot][atom] (row stride 65 words, so a record's scattered
+// slots and a slot row's consecutive atoms both spread over the banks), with
+// coalesced 16-B record accesses on one side and coalesced bank rows on the other.
+constexpr int kBankAtoms = 64, kBankThreads = 256, kBankStride = 65;
+
+__global__ void __launch_bounds__(kBankThreads)
+    bank_from_states_kernel(const ranmar_state* __restrict__ st, uint64_t n,
+                            uint32_t* __restrict__ bank, uint32_t* status) {
+    __shared__ uint32_t tile[99 * kBankStride];  // slots 0..96, v, cursor
+    __shared__ int ics[kBankAtoms];
+    const int t = threadIdx.x;
+    const uint64_t a0 = static_cast<uint64_t>(blockIdx.x) * kBankAtoms;
+    const int cnt = n - a0 < static_cast<uint64_t>(kBankAtoms) ? static_cast<int>(n - a0) : kBankAtoms;
+    if (t < cnt) {
+        const ranmar_state* r = st + a0 + t;
+        const int i0 = r->i;
+        if (!state_ok(i0, r->j, r->v)) atomicOr(status, kStatusBadState);
+        const int ic = static_cast<unsigned>(i0) < 97u ? i0 : 0;
+        ics[t] = ic;
+        tile[97 * kBankStride + t] = r->v;
+        tile[98 * kBankStride + t] = static_cast<uint32_t>(ic);
     }
-    bank[97 * n + a] = r->v;
-    bank[98 * n + a] = static_cast<uint32_t>(ic);
+    __syncthreads();
+    // record word w of atom a goes to slot (ic - w) mod 97 (canonical order)
+    const uint4* src = reinterpret_cast<const uint4*>(st + a0);
+    for (int u = t; u < cnt * 25; u += kBankThreads) {
+        const int a = u / 25, c = u - 25 * a;
+        const uint4 x = src[u];
+        int sl = ics[a] - 4 * c;
+        sl += sl < 0 ? 97 : 0;
+        tile[sl * kBankStride + a] = x.x;
+        if (c < 24) {
+            sl = sl == 0 ? 96 : sl - 1;
+            tile[sl * kBankStride + a] = x.y;
+            sl = sl == 0 ? 96 : sl - 1;
+            tile[sl * kBankStride + a] = x.z;
+            sl = sl == 0 ? 96 : sl - 1;
+            tile[sl * kBankStride + a] = x.w;
+        }
+    }
+    __syncthreads();
+    for (int x = t; x < 99 * kBankAtoms; x += kBankThreads) {
+        const int sl = x / kBankAtoms, a = x - sl * kBankAtoms;
+        if (a < cnt) bank[sl * n + a0 + a] = tile[sl * kBankStride + a];
+    }
 }
 
-__global__ void bank_to_states_kernel(const uint32_t* __restrict__ bank, uint64_t n, uint32_t t97,
-                                      ranmar_state* __restrict__ st) {
-    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n) return;
-    ranmar_state* r = st + a;
-    const int i0 = static_cast<int>(bank[98 * n + a]);
-#pragma unroll 4
-    for (int s = 0; s < 97; ++s) {
-        const int q = i0 - s;
-        r->lane[q < 0 ? q + 97 : q] = bank[s * n + a] & kMask;
+__global__ void __launch_bounds__(kBankThreads)
+    bank_to_states_kernel(const uint32_t* __restrict__ bank, uint64_t n, uint32_t t97,
+                          ranmar_state* __restrict__ st) {
+    __shared__ uint32_t tile[99 * kBankStride];
+    const int t = threadIdx.x;
+    const uint64_t a0 = static_cast<uint64_t>(blockIdx.x) * kBankAtoms;
+    const int cnt = n - a0 < static_cast<uint64_t>(kBankAtoms) ? static_cast<int>(n - a0) : kBankAtoms;
+    for (int x = t; x < 99 * kBankAtoms; x += kBankThreads) {
+        const int sl = x / kBankAtoms, a = x - sl * kBankAtoms;
+        if (a < cnt) tile[sl * kBankStride + a] = bank[sl * n + a0 + a];
     }
-    int i = i0 - static_cast<int>(t97);
-    i += i < 0 ? 97 : 0;
-    r->i = i;
-    r->j = i >= 64 ? i - 64 : i + 33;
-    r->v = bank[97 * n + a];
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(st + a0);
+    for (int u = t; u < cnt * 25; u += kBankThreads) {
+        const int a = u / 25, c = u - 25 * a;
+        const int ic = static_cast<int>(tile[98 * kBankStride + a]);
+        int sl = ic - 4 * c;
+        sl += sl < 0 ? 97 : 0;
+        uint4 x;
+        x.x = tile[sl * kBankStride + a] & kMask;
+        if (c < 24) {
+            sl = sl == 0 ? 96 : sl - 1;
+            x.y = tile[sl * kBankStride + a] & kMask;
+            sl = sl == 0 ? 96 : sl - 1;
+            x.z = tile[sl * kBankStride + a] & kMask;
+            sl = sl == 0 ? 96 : sl - 1;
+            x.w = tile[sl * kBankStride + a] & kMask;
+        } else {  // word 96, then the cursors after t steps and v
+            int i = ic - static_cast<int>(t97);
+            i += i < 0 ? 97 : 0;
+            x.y = static_cast<uint32_t>(i);
+            x.z = static_cast<uint32_t>(i >= 64 ? i - 64 : i + 33);
+            x.w = tile[97 * kBankStride + a];
+        }
+        dst[u] = x;
+    }
 }
 
 // Uniform-noise Langevin on a bank: every stream draws 3 outputs (an atom with
@@ -312,8 +363,8 @@ cudaError_t launch_bank_from_states(const ranmar_state* d_states, uint64_t n, ui
                                    uint32_t* status, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     count_launch();
-    bank_from_states_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
-        d_states, n, d_bank, status);
+    bank_from_states_kernel<<<static_cast<unsigned>((n + kBankAtoms - 1) / kBankAtoms), kBankThreads, 0,
+                              stream>>>(d_states, n, d_bank, status);
     return cudaGetLastError();
 }
 
@@ -321,8 +372,8 @@ cudaError_t launch_bank_to_states(const uint32_t* d_bank, uint64_t n, uint64_t t
                                   ranmar_state* d_states, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     count_launch();
-    bank_to_states_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
-        d_bank, n, static_cast<uint32_t>(t % 97), d_states);
+    bank_to_states_kernel<<<static_cast<unsigned>((n + kBankAtoms - 1) / kBankAtoms), kBankThreads, 0,
+                            stream>>>(d_bank, n, static_cast<uint32_t>(t % 97), d_states);
     return cudaGetLastError();
 }
 
