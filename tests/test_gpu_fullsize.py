@@ -42,7 +42,18 @@ def test_config5_full(oracle):
     d = rb.make_streams(7, j, n)
     g = rb.gauss_states_from(d)
     del d
+    g0 = g.clone()
     out = rb.gaussian(g, per, steps)
+    # the in-kernel moments consumer on the same start states: the same final states, and
+    # per atom the sequential sums of exactly the deviates gaussian() stored
+    mom = rb.gaussian_moments(g0, per * steps)
+    assert torch.equal(g0, g)
+    rng = np.random.default_rng(5)
+    for k in [0, n - 1] + list(rng.integers(0, n, 254)):
+        x = out[:, k, :].cpu().numpy().reshape(-1)
+        mk = mom[k].cpu().numpy()
+        assert mk[0] == np.cumsum(x)[-1] and mk[1] == np.cumsum(x * x)[-1], k
+    del g0, mom
     assert torch.isfinite(out).all()
     base = oracle.init(7)
     gh = g.cpu().numpy().view(GAUSS_DTYPE).reshape(-1)
