@@ -285,9 +285,14 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
 // (warp per entry); Tab_0 and Tab_1 also written transposed for the bulk kernels.
 // One CTA per entry: its <= 6 products run at CTA speed (the chain is the
 // latency of the whole setup, not the few MACs).
+// With put_dst set, block 0 also writes the host-given base state `put` to
+// put_dst (the launch that would otherwise be put_state_kernel's).
 __global__ void __launch_bounds__(256)
     tables_kernel(const uint32_t* __restrict__ Q, uint32_t* __restrict__ Tab,
-                  uint32_t* __restrict__ Tt) {
+                  uint32_t* __restrict__ Tt, const __grid_constant__ ranmar_state put,
+                  ranmar_state* __restrict__ put_dst) {
+    if (put_dst && blockIdx.x == 0 && threadIdx.x < 100)
+        reinterpret_cast<uint32_t*>(put_dst)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&put)[threadIdx.x];
     __shared__ uint32_t f[7][kPolyN];  // the entry's factors, fetched together up front
     __shared__ uint32_t acc[kPolyN];
     __shared__ BlockMulScratch scr;
@@ -563,11 +568,6 @@ __global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13) * JS)
     }
 }
 
-__global__ void put_state_kernel(ranmar_state s, ranmar_state* dst) {
-    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&s);
-    for (int k = threadIdx.x; k < 100; k += blockDim.x) d[k] = src[k];
-}
 
 // A device-resident base state copied into the workspace and checked there
 // (the host path checks it before launching): cursors, v and every lane must
@@ -1513,9 +1513,11 @@ cudaError_t launch_pow_table(const uint64_t (*e)[4], const int* shift, uint32_t*
 }
 
 cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t* Tt,
-                          cudaStream_t stream) {
+                          const ranmar_state* put, ranmar_state* put_dst, cudaStream_t stream) {
     count_launch();
-    tables_kernel<<<levels * kRows, 256, 0, stream>>>(Q, Tab, Tt);
+    ranmar_state pv{};
+    if (put) pv = *put;
+    tables_kernel<<<levels * kRows, 256, 0, stream>>>(Q, Tab, Tt, pv, put ? put_dst : nullptr);
     return cudaGetLastError();
 }
 
@@ -1583,11 +1585,6 @@ cudaError_t launch_level(const ranmar_state* in, uint64_t count, const uint32_t*
     return cudaGetLastError();
 }
 
-cudaError_t launch_put_state(const ranmar_state& s, ranmar_state* dst, cudaStream_t stream) {
-    count_launch();
-    put_state_kernel<<<1, 128, 0, stream>>>(s, dst);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_copy_state(const ranmar_state* src, ranmar_state* dst, uint32_t* status,
                               cudaStream_t stream) {

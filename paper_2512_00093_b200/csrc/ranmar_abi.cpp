@@ -68,12 +68,12 @@ cudaError_t launch_crlog_sweep(uint64_t, uint64_t, int, unsigned long long*, uin
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
                              const uint32_t*, cudaStream_t);
-cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, cudaStream_t);
+cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, const ranmar_state*, ranmar_state*,
+                          cudaStream_t);
 cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
                          uint32_t*, int, cudaStream_t);
 cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
                          uint32_t*, uint32_t*, cudaStream_t);
-cudaError_t launch_put_state(const ranmar_state&, ranmar_state*, cudaStream_t);
 cudaError_t launch_copy_state(const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
 cudaError_t launch_level_tc(const uint32_t*, uint64_t, const uint32_t*, uint64_t, uint32_t,
                             const ranmar_state*, uint32_t*, uint32_t*, uint32_t*, int, cudaStream_t);
@@ -619,11 +619,12 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     }
     if (njobs) RB_CUDA(rb::launch_pow_table(e, shift, outs, njobs, Z, s), "pow_table_kernel launch");
     // Offset tables Tab_L[r] = P_{r 128^L J}.
-    RB_CUDA(rb::launch_tables(Qsrc, p.tab_levels, Tab, Tt, s), "tables_kernel launch");
-    // The base state, in the workspace; A_0 = s_{first J}.
-    if (h_base) {
-        RB_CUDA(rb::launch_put_state(*h_base, dbase, s), "put_state launch");
-    } else {
+    // (a host-given base state rides along as a kernel parameter and is written
+    // into the workspace by the same launch)
+    RB_CUDA(rb::launch_tables(Qsrc, p.tab_levels, Tab, Tt, h_base, dbase, s), "tables_kernel launch");
+    // The base state, in the workspace (a host-given one was written by tables_kernel);
+    // A_0 = s_{first J}.
+    if (!h_base) {
         RB_CUDA(rb::launch_copy_state(d_base, dbase, status, s), "copy_state launch");
     }
     const uint32_t jm = mod_u32(J, kMod);
