@@ -1226,7 +1226,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bulk_tc_kernel(const __grid_con
 // shared memory, six u8 x u8 -> s32 GEMMs of 128 x 112 x 224 per tile, exact
 // as in bulk_tc_kernel. One 16-warp CTA per SM; warps w, w + 4, w + 8, w + 12
 // share the tile's states 32 w .. 32 w + 31 (their TMEM lane quarter) and split
-// each phase.
+// each phase; once a tile's MMAs completed, warps 0-7 read it back while warps
+// 8-15 already pack the next tile into TMEM (2^20 jumps: 0.394 -> 0.359 ms).
 constexpr int kAtThreads = 512;                       // four warps per TMEM lane quarter
 constexpr int kAtWq = kAtThreads / 128;               // warps per quarter
 constexpr int kAtN = 112;
@@ -1383,50 +1384,78 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         return hdr;
     };
 
-    uint4 hdr_next = make_uint4(0u, 96u, 32u, 0u);
-    if (blockIdx.x < n_tiles) hdr_next = prep(blockIdx.x, 0);
-    // Per tile: pack its rows into TMEM, issue its MMAs, prepare the next tile in
-    // shared memory while the tensor core runs, then read this tile back.
-    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, phase ^= 1u) {
-        const uint64_t sb = tile * 128;
-        const uint64_t srow = sb + row;
-        const bool live = srow < n;
-        const uint4 hdr = hdr_next;
-        // 2. this thread's row as u8 limbs into TMEM: limb a, K-step ks at tmA + (7 a + ks) 8
-        // (K-steps 2 sub, 2 sub + 1 by warp `sub` of the quarter)
-        {
-            const uint4* Wr4 = reinterpret_cast<const uint4*>(W + row * kAtWStride);
+    // this thread's row of the tile in W as u8 limbs into TMEM: limb a, K-step ks at
+    // tmA + (7 a + ks) 8, K-steps ks0, ks0 + kstep, ...
+    auto pack = [&](int ks0, int kstep) {
+        const uint4* Wr4 = reinterpret_cast<const uint4*>(W + row * kAtWStride);
 #pragma unroll 1
-            for (int ks = 2 * sub; ks < (2 * sub + 2 < kAtKSteps ? 2 * sub + 2 : kAtKSteps); ++ks) {
-                uint32_t v[32];
+        for (int ks = ks0; ks < kAtKSteps; ks += kstep) {
+            uint32_t v[32];
 #pragma unroll
-                for (int e4 = 0; e4 < 8; ++e4) {
-                    uint4 x = make_uint4(0u, 0u, 0u, 0u);
-                    if (8 * ks + e4 < kAtWStride / 4) x = Wr4[8 * ks + e4];
-                    v[4 * e4] = x.x;
-                    v[4 * e4 + 1] = x.y;
-                    v[4 * e4 + 2] = x.z;
-                    v[4 * e4 + 3] = x.w;
-                }
-                uint32_t q[3][8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    limbs3(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], q[0][c], q[1][c], q[2][c]);
-#pragma unroll
-                for (uint32_t a = 0; a < 3; ++a)
-                    asm volatile(
-                        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                            tmA + tq + (a * kAtKSteps + ks) * 8),
-                        "r"(q[a][0]), "r"(q[a][1]), "r"(q[a][2]), "r"(q[a][3]), "r"(q[a][4]), "r"(q[a][5]),
-                        "r"(q[a][6]), "r"(q[a][7])
-                        : "memory");
+            for (int e4 = 0; e4 < 8; ++e4) {
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if (8 * ks + e4 < kAtWStride / 4) x = Wr4[8 * ks + e4];
+                v[4 * e4] = x.x;
+                v[4 * e4 + 1] = x.y;
+                v[4 * e4 + 2] = x.z;
+                v[4 * e4 + 3] = x.w;
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            uint32_t q[3][8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                limbs3(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3], q[0][c], q[1][c], q[2][c]);
+#pragma unroll
+            for (uint32_t a = 0; a < 3; ++a)
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                        tmA + tq + (a * kAtKSteps + ks) * 8),
+                    "r"(q[a][0]), "r"(q[a][1]), "r"(q[a][2]), "r"(q[a][3]), "r"(q[a][4]), "r"(q[a][5]),
+                    "r"(q[a][6]), "r"(q[a][7])
+                    : "memory");
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    };
+    // read back chunks c0, c0 + cstep, ... of this thread's row, combine the limbs,
+    // decanonicalize (jump.hpp:42-48): column m~ of chunk c is word m~ - 12 -> groups
+    // 4 c - 3 + q hold val[4 q .. 4 q + 3]
+    auto readback = [&](uint64_t tile, const uint4 hdr, int c0, int cstep) {
+        const uint64_t srow = tile * 128 + row;
+        const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(hdr.w) + (kMod - dec)) % kMod);
+        uint4* dst = srow < n ? reinterpret_cast<uint4*>(out[srow].lane) : nullptr;
+#pragma unroll 1
+        for (int c = c0; c < 7; c += cstep) {
+            uint32_t val[16];
+            tc_read_chunk<kAtN>(tm + tq + 16 * c, val);
+            if (dst) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int g = 4 * c - 3 + q;
+                    if (g < 0) continue;
+                    const uint4 x = g == 24 ? make_uint4(val[12], 96u, 32u, v)
+                                            : make_uint4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
+                    __stcs(dst + g, x);
+                }
+            }
+        }
+    };
+
+    uint4 hdr_next = make_uint4(0u, 96u, 32u, 0u);
+    if (blockIdx.x < n_tiles) {
+        hdr_next = prep(blockIdx.x, 0);
+        pack(sub, 4);  // the first tile: K-steps sub, sub + 4 on all 16 warps
+    }
+    // Per tile: issue its MMAs, prepare the next tile in shared memory while the
+    // tensor core runs, then, once the MMAs are done, read this tile back (warps
+    // 0-7) while the next tile's rows are packed into TMEM (warps 8-15): the
+    // accumulators and the A operand are disjoint TMEM columns, and the A operand
+    // is free as soon as this tile's MMAs completed.
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, phase ^= 1u) {
+        const uint4 hdr = hdr_next;
+        const bool has_next = tile + gridDim.x < n_tiles;
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // 3. D0 = A0 B0, D1 = A0 B1 + A1 B0, D2 = A0 B2 + A1 B1 + A2 B0 (K = 224 in 7 steps)
+        // D0 = A0 B0, D1 = A0 B1 + A1 B0, D2 = A0 B2 + A1 B1 + A2 B0 (K = 224 in 7 steps)
         if (warp == 0) {  // converged warp, elect.sync issues (constant operands)
             constexpr uint32_t ta[6] = {0, 0, 1, 0, 1, 2}, tb[6] = {0, 1, 0, 2, 1, 0}, td[6] = {0, 1, 1, 2, 2, 2};
 #pragma unroll
@@ -1448,32 +1477,16 @@ __global__ void __launch_bounds__(kAtThreads, 1)
                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar)
                 : "memory");
         }
-        if (tile + gridDim.x < n_tiles) hdr_next = prep(tile + gridDim.x, phase ^ 1u);
+        if (has_next) hdr_next = prep(tile + gridDim.x, phase ^ 1u);
         mbar_wait_a(bar, phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // 4. read back, combine the limbs, decanonicalize (jump.hpp:42-48): column m~
-        // of chunk c is word m~ - 12 -> groups 4 c - 3 + q hold val[4 q .. 4 q + 3]
-        const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(hdr.w) + (kMod - dec)) % kMod);
-        uint4* dst = live ? reinterpret_cast<uint4*>(out[srow].lane) : nullptr;
-#pragma unroll
-        for (int c = 2 * sub; c < (2 * sub + 2 < 7 ? 2 * sub + 2 : 7); ++c) {
-            uint32_t val[16];
-            tc_read_chunk<kAtN>(tm + tq + 16 * c, val);
-            if (dst) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int g = 4 * c - 3 + q;
-                    if (g < 0) continue;
-                    const uint4 x = g == 24 ? make_uint4(val[12], 96u, 32u, v)
-                                            : make_uint4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
-                    __stcs(dst + g, x);
-                }
-            }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // accumulators and the W rows are free for the next tile
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (sub < 2)
+            readback(tile, hdr, sub, 2);
+        else if (has_next)
+            pack(sub - 2, 2);
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
