@@ -1332,24 +1332,30 @@ __global__ void __launch_bounds__(kAtThreads, 1)
         if (sub == 0) ci[row] = i0;
         __syncthreads();
 #pragma unroll 4
-        for (int u = t; u < 128 * 25; u += kAtThreads) {
-            const int st = u / 25, q0 = 4 * (u - 25 * st);  // state, first word
-            const int ri = ci[st];
-            uint4 x = make_uint4(0u, 0u, 0u, 0u);
-            if (static_cast<uint64_t>(st) < rows_here) x = raw4[u];
+        {   // thread (state st = t / 4, part t % 4) re-lays chunks part, part + 4, ... of st
+            const int st = t >> 2, part = t & 3;
+            const bool in_tile = static_cast<uint64_t>(st) < rows_here;
             uint32_t* Wr = W + st * kAtWStride;
-            int k = ri - q0;  // canonical index of word q0
+            const uint4* rs = raw4 + 25 * st;
+            int k = ci[st] - 4 * part;  // canonical index of the chunk's first word
             k += k < 0 ? 97 : 0;
-            Wr[k] = x.x;
-            bad |= x.x > kMask;
-            if (q0 < 96) {
-                k = k == 0 ? 96 : k - 1;
-                Wr[k] = x.y;
-                k = k == 0 ? 96 : k - 1;
-                Wr[k] = x.z;
-                k = k == 0 ? 96 : k - 1;
-                Wr[k] = x.w;
-                bad |= (x.y | x.z | x.w) > kMask;
+#pragma unroll
+            for (int c = part; c < 25; c += 4) {
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if (in_tile) x = rs[c];
+                Wr[k] = x.x;
+                bad |= x.x > kMask;
+                if (c < 24) {
+                    int k1 = k == 0 ? 96 : k - 1;
+                    Wr[k1] = x.y;
+                    k1 = k1 == 0 ? 96 : k1 - 1;
+                    Wr[k1] = x.z;
+                    k1 = k1 == 0 ? 96 : k1 - 1;
+                    Wr[k1] = x.w;
+                    bad |= (x.y | x.z | x.w) > kMask;
+                }
+                k -= 16;  // the next chunk of this thread: 4 chunks = 16 words on
+                k += k < 0 ? 97 : 0;
             }
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, kStatusBadState);
