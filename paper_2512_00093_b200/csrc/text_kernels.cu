@@ -3,11 +3,13 @@
 // stream starts made on the GPU (e.g. config 3's 2^20) can be exported and
 // re-imported in the reference's "ranmar24 v1" text without a CPU loop.
 //
-//   text_len_kernel    thread per state: exact byte length of its text
-//   scan kernels       exclusive prefix sum of the lengths -> offsets
-//   to_text_kernel     warp per state: lane-parallel line formatting, the
-//                      line offsets by a warp prefix sum
-//   from_text_kernel   thread per state: the reference's strict parser
+//   to_text_kernel     one pass, warp per state, 8 states per CTA: lines
+//                      formatted in registers, the CTA's byte offset found
+//                      by a decoupled look-back over the preceding CTAs'
+//                      totals (no separate length / scan kernels), the
+//                      texts assembled in shared memory and stored 16 B at
+//                      a time; writes the offsets too
+//   from_text_warp_kernel  warp per state: the reference's strict parser
 //                      (same checks, same 1-based line numbers in the error)
 #include <cstdint>
 
@@ -17,244 +19,278 @@ namespace rb {
 
 namespace {
 
-// Decimal digits of x: independent compares instead of a division chain.
-__device__ __forceinline__ int ndigits(uint32_t x) {
-    return 1 + (x >= 10u) + (x >= 100u) + (x >= 1000u) + (x >= 10000u) + (x >= 100000u) +
-           (x >= 1000000u) + (x >= 10000000u) + (x >= 100000000u) + (x >= 1000000000u);
-}
-
-// x in decimal at p (no terminator); returns the end. The low and high 4-digit
-// groups are converted by two independent chains.
-__device__ __forceinline__ char* put_uint(char* p, uint32_t x) {
-    const int d = ndigits(x);
-    uint32_t hi = x / 10000u, lo = x - hi * 10000u;
-    char* e = p + d;
-    int k = d - 1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // the low group (digits d-1 .. d-4)
-        if (k < 0) break;
-        const uint32_t t = lo / 10u;
-        p[k--] = static_cast<char>('0' + (lo - 10u * t));
-        lo = t;
-    }
-    while (k >= 0) {  // the high group (at most 6 more digits)
-        const uint32_t t = hi / 10u;
-        p[k--] = static_cast<char>('0' + (hi - 10u * t));
-        hi = t;
-    }
-    return e;
-}
-
-// serialize.hpp:21-40 line by line: 0 "ranmar24 v1", 1 "i <i+1> j <j+1>",
-// 2 "v <v>", 3 + k "u <k+1> <lane[k]>".
-__device__ __forceinline__ int line_len(const ranmar_state& s, int line) {
-    if (line == 0) return 12;
-    if (line == 1) return 2 + ndigits(s.i + 1) + 3 + ndigits(s.j + 1) + 1;
-    if (line == 2) return 2 + ndigits(s.v) + 1;
-    const int k = line - 3;  // k + 1 <= 97: at most two digits
-    return 2 + (k + 1 >= 10 ? 2 : 1) + 1 + ndigits(s.lane[k]) + 1;
-}
-
-// "u <k+1> <x>\n" for x < 10^8 without loops or data-dependent branches: the
-// eight decimal digits come from two 4-digit groups by multiply-high, the
-// leading zeros are skipped by predicated byte stores (the generic put_uint
-// loops cost ~4x the instructions, and this line is 97 of every state's 100).
-__device__ __forceinline__ void put_u_line(char* p, uint32_t k1, uint32_t x) {
-    p[0] = 'u';
-    p[1] = ' ';
-    const bool two = k1 >= 10u;
-    const uint32_t kt = k1 / 10u;
-    p[2] = static_cast<char>('0' + (two ? kt : k1));
-    if (two) p[3] = static_cast<char>('0' + (k1 - 10u * kt));
-    char* q = p + (two ? 4 : 3);
-    *q++ = ' ';
-    const int d = ndigits(x);  // 1..8
+// x < 10^8 in decimal as up to 8 ASCII bytes of a u64 (byte 0 = the first
+// character), d = its digit count. The two 4-digit groups are split into
+// digits by SWAR multiply-shifts (two 16-bit lanes per u32, then bytes), the
+// leading zeros are dropped by one shift: no loop, no division chain, no
+// per-byte store.
+__device__ __forceinline__ uint64_t dec8(uint32_t x, int& d) {
     const uint32_t hi = x / 10000u, lo = x - 10000u * hi;
-    uint32_t dig[8];
-    {
-        const uint32_t h1 = hi / 100u, h0 = hi - 100u * h1, l1 = lo / 100u, l0 = lo - 100u * l1;
-        const uint32_t g[4] = {h1, h0, l1, l0};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const uint32_t t = g[c] / 10u;
-            dig[2 * c] = t;
-            dig[2 * c + 1] = g[c] - 10u * t;
-        }
-    }
-    char* z = q - (8 - d);  // digit i of the 8 lands at z + i
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (i >= 8 - d) z[i] = static_cast<char>('0' + dig[i]);
-    q[d] = '\n';
+    auto split = [](uint32_t g) -> uint32_t {  // g < 10^4 -> 4 digit bytes
+        const uint32_t q = (g * 5243u) >> 19;    // g / 100 (exact for g < 43699)
+        const uint32_t w = q | ((g - 100u * q) << 16);
+        const uint32_t t = ((w * 103u) >> 10) & 0x000F000Fu;  // each lane / 10 (lanes < 100)
+        return t | ((w - 10u * t) << 8);
+    };
+    const uint64_t D = split(hi) | (static_cast<uint64_t>(split(lo)) << 32);
+    const int lz = min(__clzll(static_cast<long long>(__brevll(D))) >> 3, 7);  // leading zero digits
+    d = 8 - lz;
+    return (D + 0x3030303030303030ull) >> (8 * lz);
 }
 
-__device__ __forceinline__ void put_line(const ranmar_state& s, int line, char* p) {
+typedef unsigned __int128 u128;
+
+// Line `line` of serialize.hpp:21-40 as bytes of a u128 (byte 0 first):
+// 0 "ranmar24 v1", 1 "i <i+1> j <j+1>", 2 "v <v>", 3 + k "u <k+1> <lane[k]>",
+// each with its '\n'. Returns the length (<= 14).
+__device__ __forceinline__ int format_line(const ranmar_state& s, int line, u128& V) {
     if (line >= 3) {
-        put_u_line(p, static_cast<uint32_t>(line - 2), s.lane[line - 3]);
-        return;
+        const uint32_t k1 = static_cast<uint32_t>(line - 2);
+        const uint32_t kt = k1 / 10u;
+        const bool two = k1 >= 10u;
+        // "u k " or "u kk "
+        const uint64_t P = two ? (0x2000002075ull | (uint64_t('0' + kt) << 16) | (uint64_t('0' + k1 - 10u * kt) << 24))
+                               : (0x20002075ull | (uint64_t('0' + k1) << 16));
+        const int pl = two ? 5 : 4;
+        int d;
+        const uint64_t D = dec8(s.lane[line - 3], d);
+        V = static_cast<u128>(P) | (static_cast<u128>(D) << (8 * pl)) | (static_cast<u128>('\n') << (8 * (pl + d)));
+        return pl + d + 1;
     }
-    if (line == 0) {
-        const char m[] = "ranmar24 v1\n";
-        for (int c = 0; c < 12; ++c) p[c] = m[c];
-        return;
+    if (line == 0) {  // "ranmar24 v1\n"
+        V = static_cast<u128>(0x343272616D6E6172ull) | (static_cast<u128>(0x0A317620ull) << 64);
+        return 12;
     }
-    if (line == 1) {
-        *p++ = 'i';
-        *p++ = ' ';
-        p = put_uint(p, static_cast<uint32_t>(s.i + 1));
-        *p++ = ' ';
-        *p++ = 'j';
-        *p++ = ' ';
-        p = put_uint(p, static_cast<uint32_t>(s.j + 1));
-        *p = '\n';
-        return;
+    if (line == 1) {  // "i a j b\n"
+        int da, db;
+        const uint64_t A = dec8(static_cast<uint32_t>(s.i + 1), da);
+        const uint64_t B = dec8(static_cast<uint32_t>(s.j + 1), db);
+        V = static_cast<u128>(0x2069u) | (static_cast<u128>(A) << 16) |
+            (static_cast<u128>(0x206A20u) << (16 + 8 * da)) | (static_cast<u128>(B) << (40 + 8 * da)) |
+            (static_cast<u128>('\n') << (40 + 8 * (da + db)));
+        return 6 + da + db;
     }
-    if (line == 2) {
-        *p++ = 'v';
-        *p++ = ' ';
-        p = put_uint(p, s.v);
-        *p = '\n';
-        return;
-    }
-    const int k = line - 3;
-    *p++ = 'u';
-    *p++ = ' ';
-    p = put_uint(p, static_cast<uint32_t>(k + 1));
-    *p++ = ' ';
-    p = put_uint(p, s.lane[k]);
-    *p = '\n';
+    int d;  // "v x\n"
+    const uint64_t D = dec8(s.v, d);
+    V = static_cast<u128>(0x2076u) | (static_cast<u128>(D) << 16) | (static_cast<u128>('\n') << (16 + 8 * d));
+    return 3 + d;
 }
 
-// warp per state (coalesced lane reads): the exact byte length of its text.
-// A state violating the reference's invariants (cursors, v, 24-bit lanes;
-// core.hpp:29-49) raises the status bit and gets an EMPTY text (length 0), so
-// text_bound() holds and no kernel writes past the caller's buffer.
-__global__ void text_len_kernel(const ranmar_state* __restrict__ st, uint64_t n,
-                                uint64_t* __restrict__ len, uint32_t* status) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int l = threadIdx.x & 31;
-    if (k >= n) return;
-    const ranmar_state& s = st[k];
-    bool bad = l == 0 && !state_ok(s.i, s.j, s.v);
-    for (int q = l; q < 97; q += 32) bad |= s.lane[q] > kMask;
-    if (__any_sync(0xffffffffu, bad)) {
-        if (l == 0) {
-            len[k] = 0;
-            atomicOr(status, kStatusBadState);
-        }
-        return;
-    }
-    uint32_t L = 0;
-#pragma unroll
-    for (int pass = 0; pass < 4; ++pass) {
-        const int line = pass * 32 + l;
-        if (line < 100) L += static_cast<uint32_t>(line_len(s, line));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    if (l == 0) len[k] = L;
-}
-
-// exclusive scan, 1024 items per block; block totals to bsum
-constexpr int kScanT = 1024;
-__global__ void __launch_bounds__(kScanT)
-    scan_block_kernel(const uint64_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ out,
-                      uint64_t* __restrict__ bsum) {
-    __shared__ uint64_t warp_tot[32];
-    const int t = threadIdx.x, l = t & 31, w = t >> 5;
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kScanT + t;
-    const uint64_t x = k < n ? in[k] : 0;
-    uint64_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (l >= o) incl += y;
-    }
-    if (l == 31) warp_tot[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        uint64_t v = warp_tot[l], wi = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (l >= o) wi += y;
-        }
-        warp_tot[l] = wi - v;  // exclusive warp offsets
-        if (l == 31 && bsum) bsum[blockIdx.x] = wi;
-    }
-    __syncthreads();
-    if (k < n) out[k] = warp_tot[w] + incl - x;
-}
-
-// out[k] += boff[block] (if any) + *base (if any); then out[n] = out[n-1] + len[n-1]
-__global__ void scan_add_kernel(uint64_t* __restrict__ out, uint64_t n,
-                                const uint64_t* __restrict__ boff, const uint64_t* base) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kScanT + threadIdx.x;
-    if (k < n) out[k] += (boff ? boff[blockIdx.x] : 0) + (base ? *base : 0);
-}
-
-__global__ void total_kernel(uint64_t* __restrict__ off, uint64_t n, const uint64_t* __restrict__ len) {
-    off[n] = off[n - 1] + len[n - 1];
-}
-
-__global__ void copy_u64_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src) {
-    *dst = *src;
+// The len (<= 14) bytes of V at byte offset p of the zero-initialised stage
+// S, as u32 words: the first and last word (shared with the neighbouring
+// lines, possibly of another warp's state) by shared-memory OR, the ones in
+// between by plain stores.
+__device__ __forceinline__ void emit_line(uint32_t* S, uint32_t p, int len, const u128& V) {
+    const uint32_t sh = 8u * (p & 3u);
+    const u128 W = V << sh;
+    const uint32_t w4 = sh ? static_cast<uint32_t>(V >> (128u - sh)) : 0u;
+    const uint32_t w0 = static_cast<uint32_t>(W), w1 = static_cast<uint32_t>(W >> 32),
+                   w2 = static_cast<uint32_t>(W >> 64), w3 = static_cast<uint32_t>(W >> 96);
+    const int nw = static_cast<int>(((p & 3u) + static_cast<uint32_t>(len) + 3u) >> 2);  // 2..5
+    uint32_t* q = S + (p >> 2);
+    atomicOr(q, w0);
+    if (nw > 2) q[1] = w1;
+    if (nw > 3) q[2] = w2;
+    if (nw > 4) q[3] = w3;
+    const uint32_t last = nw == 2 ? w1 : nw == 3 ? w2 : nw == 4 ? w3 : w4;
+    atomicOr(q + nw - 1, last);
 }
 
 // Upper bound of one state's text: 12 + 10 + 11 + 97 * 14.
 constexpr uint64_t kMaxStateText = 12 + 10 + 11 + 97 * 14;
 constexpr int kTTStates = 8;  // states (warps) per CTA
-constexpr int kTTStage = kTTStates * static_cast<int>(kMaxStateText) + 16;
+constexpr int kTTStage = (kTTStates * static_cast<int>(kMaxStateText) + 16 + 15) & ~15;
 
-// Warp per state: lane handles lines lane, lane+32, lane+64, lane+96, the
-// line offsets by a warp prefix sum. The CTA's 8 consecutive texts are
-// formatted into shared memory, placed at the same offset mod 16 as in the
-// output, and then written out as aligned 16-B stores (byte stores only for
-// the unaligned head and tail of the CTA's range).
+// "u <k1> <x>\n" (k1 <= 97, x <= kMask) at byte offset p of the zeroed stage
+// S, built as u32 words: the prefix "u k1 " shifted by p & 3, the digits of
+// x (dec8) with the '\n' after them shifted by (p & 3) + the prefix length
+// with funnel shifts, first and last word by shared-memory OR (shared with
+// the neighbouring lines), the words between by plain stores. Returns the
+// line's length. format (emit = false) only returns the length.
+__device__ __forceinline__ uint32_t u_line_len(uint32_t k1, int d) { return (k1 >= 10u ? 6u : 5u) + d; }
+
+__device__ __forceinline__ void emit_u_line(uint32_t* S, uint32_t p, uint32_t k1, uint64_t D, int d) {
+    const uint32_t s = p & 3u;
+    const uint32_t kt = k1 / 10u;
+    const bool two = k1 >= 10u;
+    const uint64_t P = two ? (0x2000002075ull | (uint64_t('0' + kt) << 16) | (uint64_t('0' + k1 - 10u * kt) << 24))
+                           : (0x20002075ull | (uint64_t('0' + k1) << 16));
+    const uint32_t pl = two ? 5u : 4u;
+    const uint64_t Ps = P << (8 * s);  // s + pl <= 8 bytes
+    const uint64_t Dn = d == 8 ? D : D | (0x0Aull << (8 * d));
+    const uint32_t r0 = static_cast<uint32_t>(Dn), r1 = static_cast<uint32_t>(Dn >> 32), r2 = d == 8 ? 0x0Au : 0u;
+    const uint32_t u = s + pl;  // 4..8 bytes: the digits start in word 1 or 2
+    const uint32_t bs = 8u * (u & 3u);
+    const uint32_t z0 = r0 << bs, z1 = __funnelshift_l(r0, r1, bs), z2 = __funnelshift_l(r1, r2, bs);
+    const bool w1 = u < 8u;
+    const uint32_t o0 = static_cast<uint32_t>(Ps);
+    const uint32_t o1 = static_cast<uint32_t>(Ps >> 32) | (w1 ? z0 : 0u);
+    const uint32_t o2 = w1 ? z1 : z0, o3 = w1 ? z2 : z1, o4 = w1 ? 0u : z2;
+    const uint32_t nw = (s + pl + static_cast<uint32_t>(d) + 4u) >> 2;  // words touched: 2..5
+    uint32_t* q = S + (p >> 2);
+    atomicOr(q, o0);
+    if (nw > 2) q[1] = o1;
+    if (nw > 3) q[2] = o2;
+    if (nw > 4) q[3] = o3;
+    const uint32_t last = nw == 2 ? o1 : nw == 3 ? o2 : nw == 4 ? o3 : o4;
+    atomicOr(q + nw - 1, last);
+}
+
+// Decoupled look-back status words, one per CTA tile: the top two bits say
+// what the low 62 hold (the tile's own byte total, or the inclusive prefix).
+constexpr uint64_t kTileAgg = 1ull << 62, kTileInc = 2ull << 62, kTileVal = kTileAgg - 1;
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One pass. Tiles of 8 states are taken in ticket order (so every earlier
+// tile is resident or done: the look-back cannot deadlock). Warp w loads its
+// state (lane l: the lanes of lines l, l+32, l+64, l+96), checks the
+// invariants (core.hpp:29-49; a bad state gets an empty text and raises the
+// status bit, so text_bound() holds) and sums its line lengths; after one
+// barrier the CTA's total is known: warp 0 publishes it and looks back 32
+// tiles at a time for the nearest inclusive prefix while all warps emit their
+// lines into the zeroed shared stage at CTA-relative offsets. After a second
+// barrier the CTA's range is stored with aligned 16-B stores (the stage read
+// at the global offset's misalignment by funnel shifts; bytes only for the
+// unaligned head and tail). tile_status[] and *ticket start zeroed.
 __global__ void __launch_bounds__(32 * kTTStates)
-    to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n,
-                   const uint64_t* __restrict__ off, char* __restrict__ text) {
+    to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n, uint64_t* __restrict__ off,
+                   char* __restrict__ text, uint64_t* tile_status, uint32_t* ticket, uint32_t* status) {
     __shared__ __align__(16) char stage[kTTStage];
-    const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kTTStates;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __shared__ uint32_t warp_len[kTTStates], warp_base[kTTStates];
+    __shared__ uint64_t s_g0;
+    __shared__ uint32_t s_tile, s_agg;
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    if (t == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int q = t; q < kTTStage / 16; q += 32 * kTTStates) reinterpret_cast<uint4*>(stage)[q] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t k0 = static_cast<uint64_t>(tile) * kTTStates;
     const uint64_t k = k0 + w;
-    const uint64_t kend = k0 + kTTStates < n ? k0 + kTTStates : n;
-    const uint64_t g0 = off[k0], g1 = off[kend];
-    const uint32_t shift = static_cast<uint32_t>(g0 & 15);
-    // (invalid states have empty texts). The warp-uniform condition predicates the
-    // work instead of branching around it: the shuffles then run in converged code
-    // (behind a branch ptxas cannot prove uniform they become WARPSYNC/collective
-    // loops).
-    const bool act = k < n && off[k + 1] != off[k];
-    const ranmar_state& s = st[act ? k : k0];
-    char* base = stage + shift + (act ? off[k] - g0 : 0);
-    uint32_t before = 0;  // bytes of the lines of previous passes
+    const bool inr = k < n;
+    const ranmar_state& s = st[inr ? k : 0];
+    uint32_t x[4];
+    bool bad = false;
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
         const int line = pass * 32 + l;
-        const bool mine = act && line < 100;
-        const uint32_t len = mine ? static_cast<uint32_t>(line_len(s, line)) : 0u;
-        uint32_t incl = len;
+        const bool u = line >= 3 && line < 100;
+        x[pass] = inr && u ? s.lane[line - 3] : 0u;
+        bad |= x[pass] > kMask;
+    }
+    bad = __any_sync(0xffffffffu, bad || (inr && l == 0 && !state_ok(s.i, s.j, s.v)));
+    if (bad && l == 0) atomicOr(status, kStatusBadState);
+    // The warp-uniform condition predicates the work instead of branching around
+    // it: the shuffles then run in converged code.
+    const bool act = inr && !bad;
+    uint64_t D[4];
+    int dg[4];
+    uint32_t incl[4], tot = 0;
+    u128 V = 0;  // header line (pass 0, lanes 0..2)
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+        const int line = pass * 32 + l;
+        D[pass] = dec8(x[pass], dg[pass]);
+        uint32_t len = 0;
+        if (act && line < 100) {
+            if (pass == 0 && l < 3)
+                len = static_cast<uint32_t>(format_line(s, line, V));
+            else
+                len = u_line_len(static_cast<uint32_t>(line - 2), dg[pass]);
+        }
+        uint32_t y = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (l >= o) incl += y;
+            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+            if (l >= o) y += z;
         }
-        if (mine) put_line(s, line, base + before + incl - len);
-        before += __shfl_sync(0xffffffffu, incl, 31);
+        incl[pass] = (tot + y) | (len << 24);  // the line's end within the state's text, and its length
+        tot += __shfl_sync(0xffffffffu, y, 31);
+    }
+    if (l == 0) warp_len[w] = tot;
+    __syncthreads();
+    uint32_t vi = 0, agg = 0;
+    if (w == 0) {  // the CTA's total and the warps' CTA-relative offsets
+        const uint32_t v = l < kTTStates ? warp_len[l] : 0u;
+        vi = v;
+#pragma unroll
+        for (int o = 1; o < kTTStates; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xffffffffu, vi, o);
+            if (l >= o) vi += z;
+        }
+        agg = __shfl_sync(0xffffffffu, vi, kTTStates - 1);
+        if (l < kTTStates) warp_base[l] = vi - v;
+        if (l == 0) st_relaxed(tile_status + tile, (tile == 0 ? kTileInc : kTileAgg) | agg);
     }
     __syncthreads();
+    {   // emit this warp's lines at their CTA-relative offsets
+        uint32_t* S = reinterpret_cast<uint32_t*>(stage);
+        const uint32_t base = warp_base[w];
+#pragma unroll
+        for (int pass = 0; pass < 4; ++pass) {
+            const uint32_t len = incl[pass] >> 24, p = base + (incl[pass] & 0xFFFFFFu) - len;
+            if (!len) continue;
+            if (pass == 0 && l < 3)
+                emit_line(S, p, static_cast<int>(len), V);
+            else
+                emit_u_line(S, p, static_cast<uint32_t>(pass * 32 + l - 2), D[pass], dg[pass]);
+        }
+    }
+    if (w == 0) {  // look-back for the tile's global offset
+        uint64_t prefix = 0;
+        if (tile != 0) {
+            int64_t j = static_cast<int64_t>(tile) - 1;  // nearest tile of the window
+            for (;;) {
+                const int64_t idx = j - l;
+                uint64_t xs = kTileInc;  // before tile 0: an inclusive 0
+                if (idx >= 0)
+                    do xs = ld_relaxed(tile_status + idx); while ((xs >> 62) == 0);
+                const uint32_t inc = __ballot_sync(0xffffffffu, (xs >> 62) == 2);
+                const int stop = inc ? __ffs(inc) - 1 : 31;  // lanes 0..stop count
+                uint64_t c = l <= stop ? (xs & kTileVal) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                prefix += c;
+                if (inc) break;
+                j -= 32;
+            }
+            if (l == 0) st_relaxed(tile_status + tile, kTileInc | (prefix + agg));
+        }
+        if (l < kTTStates && k0 + l < n) off[k0 + l] = prefix + warp_base[l];
+        if (l == 0) {
+            s_g0 = prefix;
+            s_agg = agg;
+            if (k0 + kTTStates >= n) off[n] = prefix + agg;  // the last tile
+        }
+    }
+    __syncthreads();
+    const uint64_t g0 = s_g0, g1 = g0 + s_agg;
     const uint64_t a = (g0 + 15) & ~uint64_t(15), b = g1 & ~uint64_t(15);
-    const int t = threadIdx.x;
     if (a >= b) {  // no aligned chunk: bytes only
-        for (uint64_t x = g0 + t; x < g1; x += blockDim.x) text[x] = stage[shift + (x - g0)];
+        for (uint32_t y = t; y < static_cast<uint32_t>(g1 - g0); y += 32 * kTTStates) text[g0 + y] = stage[y];
         return;
     }
-    if (g0 + t < a) text[g0 + t] = stage[shift + t];
-    if (b + t < g1) text[b + t] = stage[shift + (b - g0) + t];
-    const uint4* src = reinterpret_cast<const uint4*>(stage + shift + (a - g0));
+    const uint32_t head = static_cast<uint32_t>(a - g0), tail0 = static_cast<uint32_t>(b - g0);
+    if (t < head) text[g0 + t] = stage[t];
+    if (tail0 + t < static_cast<uint32_t>(g1 - g0)) text[b + t] = stage[tail0 + t];
+    // aligned chunk c of the output = stage bytes [head + 16 c, +16): 5 words, funnel-shifted
+    const uint32_t* S = reinterpret_cast<const uint32_t*>(stage);
+    const uint32_t sb = 8u * (head & 3u), w0 = head >> 2;
     uint4* dst = reinterpret_cast<uint4*>(text + a);
-    for (uint64_t q = t; q < (b - a) / 16; q += blockDim.x) dst[q] = src[q];
+    const uint32_t nchunks = static_cast<uint32_t>((b - a) >> 4);
+    for (uint32_t c = t; c < nchunks; c += 32 * kTTStates) {
+        const uint32_t* q = S + w0 + 4 * c;
+        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3], v4 = q[4];
+        dst[c] = make_uint4(__funnelshift_r(v0, v1, sb), __funnelshift_r(v1, v2, sb), __funnelshift_r(v2, v3, sb),
+                            __funnelshift_r(v3, v4, sb));
+    }
 }
 
 // ---- parser (serialize.hpp:81-136), thread per state
@@ -358,10 +394,68 @@ __device__ __forceinline__ bool num_at(const char* sm, int& p, int e, uint64_t& 
     return nd > 0;
 }
 
-__global__ void __launch_bounds__(32 * kFTWarps)
+// 16-bit mask of the '\n' bytes of a 16-B chunk (bit i = byte i): exact
+// zero-byte test of x ^ 0x0A0A0A0A per word, bytes gathered by a multiply.
+__device__ __forceinline__ uint32_t nl_nibble(uint32_t x) {
+    const uint32_t y = x ^ 0x0A0A0A0Au;
+    const uint32_t z = ~(((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y | 0x7F7F7F7Fu);  // 0x80 where zero
+    return ((z >> 7) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t nl_mask16(uint4 c) {
+    return nl_nibble(c.x) | (nl_nibble(c.y) << 4) | (nl_nibble(c.z) << 8) | (nl_nibble(c.w) << 12);
+}
+
+// 16 bytes of the warp's stage from byte q (word view S, readable to q + 20)
+__device__ __forceinline__ void load16(const uint32_t* S, int q, uint64_t& lo, uint64_t& hi) {
+    const uint32_t* W = S + (q >> 2);
+    const uint32_t sh = 8u * (q & 3);
+    const uint32_t w0 = W[0], w1 = W[1], w2 = W[2], w3 = W[3], w4 = W[4];
+    lo = __funnelshift_r(w0, w1, sh) | (static_cast<uint64_t>(__funnelshift_r(w1, w2, sh)) << 32);
+    hi = __funnelshift_r(w2, w3, sh) | (static_cast<uint64_t>(__funnelshift_r(w3, w4, sh)) << 32);
+}
+
+// A line in canonical "<prefix><digits>" form: the pl-byte prefix P exactly,
+// then 1..8 digits and nothing else. Returns false for anything else (left to
+// the character-level checks, which also decide leading zeros, other
+// separators, overflow and junk), else the number (<= 99999999, so the
+// reference's 2^32 - 1 overflow check cannot fire). The line is [q, q+L) of
+// the warp's stage.
+__device__ __forceinline__ bool parse_num_fast(const uint32_t* S, int q, int L, uint64_t P, int pl, uint32_t& val) {
+    const int nd = L - pl;
+    if (nd < 1 || nd > 8) return false;
+    uint64_t lo, hi;
+    load16(S, q, lo, hi);
+    if ((lo & ((1ull << (8 * pl)) - 1)) != P) return false;
+    const uint64_t M = nd == 8 ? ~0ull : (1ull << (8 * nd)) - 1;
+    const uint64_t D = ((lo >> (8 * pl)) | (hi << (64 - 8 * pl))) & M;  // the digit bytes, first at byte 0
+    constexpr uint64_t H = 0x8080808080808080ull;
+    const uint64_t ge0 = ((D | H) - 0x3030303030303030ull) & H;   // (c & 0x7F) >= '0'
+    const uint64_t gt9 = ((D & ~H) + 0x4646464646464646ull) & H;  // (c & 0x7F) > '9'
+    if ((ge0 & ~gt9 & ~D & M & H) != (M & H)) return false;
+    uint64_t x = (D - (0x3030303030303030ull & M)) << (8 * (8 - nd));  // right-aligned digit values
+    x = ((x & 0x0F0F0F0F0F0F0F0Full) * 2561) >> 8;                // pairs
+    x = ((x & 0x00FF00FF00FF00FFull) * 6553601) >> 16;            // groups of 4
+    x = ((x & 0x0000FFFF0000FFFFull) * 42949672960001ull) >> 32;  // 8 digits
+    val = static_cast<uint32_t>(x);
+    return true;
+}
+
+// Line "u <k1> <x>" (serialize.hpp:115-126) in canonical form: 1 (x <= kMask,
+// lane = x), 0 (x > kMask: the reference fails on this line), -1 (not
+// canonical: the character-level checks decide).
+__device__ __forceinline__ int parse_u_fast(const uint32_t* S, int q, int L, uint32_t k1, uint32_t& lane) {
+    const uint32_t kt = k1 / 10u;
+    const bool two = k1 >= 10u;
+    const uint64_t P = two ? (0x2000002075ull | (uint64_t('0' + kt) << 16) | (uint64_t('0' + k1 - 10u * kt) << 24))
+                           : (0x20002075ull | (uint64_t('0' + k1) << 16));
+    if (!parse_num_fast(S, q, L, P, two ? 5 : 4, lane)) return -1;
+    return lane <= kMask ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(32 * kFTWarps, 12)
     from_text_warp_kernel(const char* __restrict__ text, const uint64_t* __restrict__ off,
                           uint64_t n, ranmar_state* __restrict__ out, int32_t* __restrict__ err) {
-    __shared__ __align__(16) char stage[kFTWarps][kFTCap + 16];
+    __shared__ __align__(16) char stage[kFTWarps][kFTCap + 32];
     __shared__ int nl[kFTWarps][kFTLines];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kFTWarps + w;
@@ -373,26 +467,44 @@ __global__ void __launch_bounds__(32 * kFTWarps)
         return;
     }
     char* sm = stage[w];
+    const uint64_t a0 = b & ~uint64_t(15);
+    const int sh = static_cast<int>(b - a0);
+    const int chunks = (sh + L + 15) >> 4;
     {   // aligned 16-B chunks covering [b, e); byte shift = b & 15
-        const uint64_t a0 = b & ~uint64_t(15);
-        const int sh = static_cast<int>(b - a0);
-        const int chunks = (sh + L + 15) >> 4;
         const uint4* src = reinterpret_cast<const uint4*>(text + a0);
         for (int q = l; q < chunks; q += 32) reinterpret_cast<uint4*>(sm)[q] = src[q];
         __syncwarp();
-        sm += sh;  // sm[0 .. L) is the text
     }
-    // newlines, in order: the warp reads 32 consecutive bytes per step (lane l
-    // byte x0 + l, conflict-free) and a ballot places the ones it finds
+    // newlines, in order: lane l tests 16-B chunk 32 r + l (one LDS.128 and a
+    // SWAR byte test), a warp scan of the counts places them
     int total_nl = 0;
-    const uint32_t lt = (1u << l) - 1u;
-    for (int x0 = 0; x0 < L && total_nl < kFTLines; x0 += 32) {
-        const bool isnl = x0 + l < L && sm[x0 + l] == '\n';
-        const uint32_t bal = __ballot_sync(0xffffffffu, isnl);
-        const int pos = total_nl + __popc(bal & lt);
-        if (isnl && pos < kFTLines) nl[w][pos] = x0 + l;
-        total_nl += __popc(bal);
+    for (int c0 = 0; c0 < chunks; c0 += 32) {
+        const int c = c0 + l;
+        uint32_t m = 0;
+        if (c < chunks) {
+            m = nl_mask16(reinterpret_cast<const uint4*>(sm)[c]);
+            const int lo = sh - 16 * c, hi = sh + L - 16 * c;  // the text's bytes [lo, hi) of the chunk
+            if (lo > 0) m &= ~((1u << lo) - 1u);
+            if (hi < 16) m &= (1u << hi) - 1u;
+        }
+        const int cnt = __popc(m);
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        int pos = total_nl + x - cnt;
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            if (pos < kFTLines) nl[w][pos] = 16 * c + bit - sh;
+            ++pos;
+            m &= m - 1;
+        }
+        total_nl += __shfl_sync(0xffffffffu, x, 31);
     }
+    const uint32_t* S = reinterpret_cast<const uint32_t*>(sm);  // word view of the stage
+    sm += sh;  // sm[0 .. L) is the text
     __syncwarp();
     // line ln (1-based) = [start, end) before '\r' stripping; exists iff start < L
     auto line_span = [&](int ln, int& st, int& en) -> bool {
@@ -414,10 +526,22 @@ __global__ void __launch_bounds__(32 * kFTWarps)
         int p, en;
         bool ok = line_span(ln, p, en);
         if (ok) {
-            if (ln == 1) {
-                const char h[] = "ranmar24 v1";
-                ok = en - p == 11;
-                for (int c = 0; ok && c < 11; ++c) ok = sm[p + c] == h[c];
+            if (ln == 1) {  // "ranmar24 v1", compared as two words
+                uint64_t lo, hi;
+                load16(S, sh + p, lo, hi);
+                ok = en - p == 11 && lo == 0x343272616D6E6172ull && (hi & 0xFFFFFFull) == 0x317620ull;
+            } else if (ln == 3) {
+                uint32_t fv;
+                if (parse_num_fast(S, sh + p, en - p, 0x2076ull, 2, fv)) {  // canonical "v <x>"
+                    ok = fv < kMod;
+                    sv = fv;
+                } else {
+                    uint64_t v = 0;
+                    ok = en - p >= 2 && sm[p] == 'v' && sm[p + 1] == ' ';
+                    p += 2;
+                    ok = ok && num_at(sm, p, en, v) && p == en && v < kMod;
+                    sv = static_cast<uint32_t>(v);
+                }
             } else if (ln == 2) {
                 uint64_t i = 0, j = 0;
                 ok = en - p >= 2 && sm[p] == 'i' && sm[p + 1] == ' ';
@@ -429,13 +553,14 @@ __global__ void __launch_bounds__(32 * kFTWarps)
                 ok = ok && i >= 1 && i <= 97 && j >= 1 && j <= 97 && (i + 97 - j) % 97 == 64;
                 si = static_cast<int32_t>(i) - 1;
                 sj = static_cast<int32_t>(j) - 1;
-            } else if (ln == 3) {
-                uint64_t v = 0;
-                ok = en - p >= 2 && sm[p] == 'v' && sm[p + 1] == ' ';
-                p += 2;
-                ok = ok && num_at(sm, p, en, v) && p == en && v < kMod;
-                sv = static_cast<uint32_t>(v);
             } else {
+                uint32_t fl;
+                const int f = parse_u_fast(S, sh + p, en - p, static_cast<uint32_t>(ln - 3), fl);
+                if (f >= 0) {
+                    vals[r] = fl;
+                    if (f == 0 && ln < bad) bad = ln;
+                    continue;
+                }
                 uint64_t idx = 0, lane = 0;
                 ok = en - p >= 2 && sm[p] == 'u' && sm[p + 1] == ' ';
                 p += 2;
@@ -484,50 +609,23 @@ __global__ void __launch_bounds__(32 * kFTWarps)
 
 uint64_t text_bound(uint64_t n) { return n * kMaxStateText; }
 
-constexpr uint64_t kTextChunk = uint64_t(kScanT) * kScanT;  // states per scan (2^20)
+static uint64_t text_tiles(uint64_t n) { return (n + kTTStates - 1) / kTTStates; }
 
-size_t text_workspace(uint64_t n) {
-    const uint64_t c = n < kTextChunk ? n : kTextChunk;
-    const uint64_t blocks = (c + kScanT - 1) / kScanT;
-    return static_cast<size_t>((c + 2 * blocks + 2) * sizeof(uint64_t));
-}
+// tile status words + the ticket counter
+size_t text_workspace(uint64_t n) { return static_cast<size_t>((text_tiles(n) + 1) * sizeof(uint64_t)); }
 
-// Offsets d_off[0..n] (d_off[n] = total bytes) and the concatenated texts;
-// chunks of 2^20 states, each continuing where the previous one ended.
+// Offsets d_off[0..n] (d_off[n] = total bytes) and the concatenated texts:
+// one memset of the look-back workspace and one kernel.
 cudaError_t launch_to_text(const ranmar_state* d_states, uint64_t n, char* d_text,
                            uint64_t* d_off, void* d_ws, uint32_t* status, cudaStream_t stream) {
-    for (uint64_t c0 = 0; c0 < n; c0 += kTextChunk) {
-        const uint64_t m = n - c0 < kTextChunk ? n - c0 : kTextChunk;
-        const uint64_t blocks = (m + kScanT - 1) / kScanT;
-        uint64_t* len = static_cast<uint64_t*>(d_ws);
-        uint64_t* bsum = len + m;
-        uint64_t* boff = bsum + blocks;
-        uint64_t* off = d_off + c0;
-        const uint64_t* base = c0 ? d_off + c0 : nullptr;  // the previous chunk's total
-        // the previous chunk wrote off[c0] = its end; keep it as this chunk's base
-        uint64_t* base_copy = boff + blocks;
-        count_launch(3);
-        text_len_kernel<<<static_cast<unsigned>((m + 7) / 8), 256, 0, stream>>>(d_states + c0, m,
-                                                                                len, status);
-        if (base) {
-            count_launch();
-            copy_u64_kernel<<<1, 1, 0, stream>>>(base_copy, base);
-        }
-        scan_block_kernel<<<static_cast<unsigned>(blocks), kScanT, 0, stream>>>(len, m, off, bsum);
-        if (blocks > 1) {
-            count_launch(2);
-            scan_block_kernel<<<1, kScanT, 0, stream>>>(bsum, blocks, boff, nullptr);
-            scan_add_kernel<<<static_cast<unsigned>(blocks), kScanT, 0, stream>>>(
-                off, m, boff, base ? base_copy : nullptr);
-        } else if (base) {
-            count_launch();
-            scan_add_kernel<<<1, kScanT, 0, stream>>>(off, m, nullptr, base_copy);
-        }
-        count_launch();
-        total_kernel<<<1, 1, 0, stream>>>(off, m, len);
-        to_text_kernel<<<static_cast<unsigned>((m + kTTStates - 1) / kTTStates), 32 * kTTStates, 0,
-                         stream>>>(d_states + c0, m, off, d_text);
-    }
+    const uint64_t tiles = text_tiles(n);
+    if (tiles > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    uint64_t* tile_status = static_cast<uint64_t*>(d_ws);
+    cudaError_t e = cudaMemsetAsync(d_ws, 0, text_workspace(n), stream);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    to_text_kernel<<<static_cast<unsigned>(tiles), 32 * kTTStates, 0, stream>>>(
+        d_states, n, d_off, d_text, tile_status, reinterpret_cast<uint32_t*>(tile_status + tiles), status);
     return cudaGetLastError();
 }
 

@@ -38,8 +38,31 @@ def test_to_text_matches_reference_format(oracle, refvec, n):
         assert texts[k] == oracle.to_text(s[k:k + 1]), k
 
 
+def test_invalid_states_across_many_tiles(oracle):
+    # empty texts for bad states (whole tiles of them too) inside a long run of
+    # tiles: the one-pass look-back must still place every valid text exactly
+    n = 5003
+    s = _random_states(n, 77)
+    bad = np.zeros(n, bool)
+    bad[::3] = True
+    bad[800:832] = True  # four whole tiles of 8
+    bad[n - 1] = True    # the last state (the total comes from the last tile)
+    s["v"][bad] = 0xFFFFFFFF
+    d = rb.states_to_device(s)
+    rb.device_status(clear=True)
+    text, off = rb.to_text_dev(d)
+    torch.cuda.synchronize()
+    assert rb.device_status(clear=True) & 1
+    o = off.cpu().numpy()
+    lens = np.diff(o)
+    assert o[0] == 0 and (lens[bad] == 0).all() and (lens[~bad] > 0).all()
+    texts = rb.texts_to_host(text, off)
+    for k in np.flatnonzero(~bad)[::37]:
+        assert texts[k] == oracle.to_text(s[k:k + 1]), k
+
+
 def test_round_trip_beyond_one_scan_chunk(oracle):
-    # > 2^20 states exercises the chunked offset scan
+    # > 2^20 states: 131,077 look-back tiles, offsets past 2^30 bytes
     n = (1 << 20) + 37
     d = rb.make_streams(31415, 2**50, n)
     text, off = rb.to_text_dev(d)
@@ -86,6 +109,29 @@ def test_from_text_errors_match_reference(refvec):
         good.replace(lines[5] + "\n", lines[5] + "\n\n"),  # an empty line inside
         "ranmar24 v1",                                 # header only
         good[:-30],                                    # cut inside the last line
+        # lines the SWAR fast path takes or hands back to the character checks
+        good.replace(lines[10], "u 8 0"),               # one digit
+        good.replace(lines[10], "u 8 00000012"),        # eight digits, leading zeros
+        good.replace(lines[10], "u 8 16777215"),        # the largest lane
+        good.replace(lines[10], "u 8 16777216"),        # eight digits, above the mask
+        good.replace(lines[10], "u 8 000000000012"),    # twelve digits, leading zeros
+        good.replace(lines[10], "u 8 123456789"),       # nine digits
+        good.replace(lines[10], "u 8 1677721a"),        # a letter among the digits
+        good.replace(lines[10], "u 8 12/"),             # '/' (just below '0')
+        good.replace(lines[10], "u 8 12:"),             # ':' (just above '9')
+        good.replace(lines[10], "u 8 1\u00b2"),        # a non-ASCII byte pair
+        good.replace(lines[10], "u 08 5"),              # index with a leading zero
+        good.replace(lines[10], "u  8 5"),              # double space before the index
+        good.replace(lines[10], "u 8\t5"),             # tab separator
+        good.replace(lines[10], "u 8 "),                # no digits
+        good.replace(lines[40], "u 38 7\r"),           # CR on a two-digit index line
+        good.replace(lines[40], "v 38 7"),              # wrong tag
+        good.replace("v 362436", "v 0362436"),         # v with a leading zero
+        good.replace("v 362436", "v 16777212"),        # the largest v
+        good.replace("v 362436", "v 3624x6"),          # v with a letter
+        good.replace("ranmar24 v1", "Ranmar24 v1"),    # header case
+        good.replace("ranmar24 v1", "ranmar24 v10"),   # header one byte long
+        good.replace("ranmar24 v1", "ranmar24 v"),     # header one byte short
     ]
     texts = [b.encode() for b in bad]
     offs = np.cumsum([0] + [len(t) for t in texts]).astype(np.int64)
@@ -95,7 +141,7 @@ def test_from_text_errors_match_reference(refvec):
     for k, b in enumerate(bad):
         assert err[k] == _host_error_line(b), (k, b[:40])
     ok = [k for k, e in enumerate(err) if e == 0]
-    assert ok == [11, 12, 14, 15, 17]
+    assert ok == [11, 12, 14, 15, 17, 21, 22, 23, 25, 31, 35, 37, 38]
     host = rb.states_to_host(states)
     for k in ok:
         assert host[k:k + 1].tobytes() == rb.from_text(bad[k]).tobytes()

@@ -1,7 +1,7 @@
 """Per-source-line totals (warp instructions, stall samples) of one kernel
 from an ncu report captured with --import-source on.
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    python tools/ncu_lines.py report.ncu-rep [top] [kernel-regex]
 """
 import collections
 import subprocess
@@ -13,7 +13,8 @@ import io
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout.splitlines()
     path = None
     agg = collections.defaultdict(lambda: [0, 0, 0, ""])
