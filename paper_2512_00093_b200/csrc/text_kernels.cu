@@ -40,40 +40,26 @@ __device__ __forceinline__ uint64_t dec8(uint32_t x, int& d) {
 
 typedef unsigned __int128 u128;
 
-// Line `line` of serialize.hpp:21-40 as bytes of a u128 (byte 0 first):
-// 0 "ranmar24 v1", 1 "i <i+1> j <j+1>", 2 "v <v>", 3 + k "u <k+1> <lane[k]>",
-// each with its '\n'. Returns the length (<= 14).
-__device__ __forceinline__ int format_line(const ranmar_state& s, int line, u128& V) {
-    if (line >= 3) {
-        const uint32_t k1 = static_cast<uint32_t>(line - 2);
-        const uint32_t kt = k1 / 10u;
-        const bool two = k1 >= 10u;
-        // "u k " or "u kk "
-        const uint64_t P = two ? (0x2000002075ull | (uint64_t('0' + kt) << 16) | (uint64_t('0' + k1 - 10u * kt) << 24))
-                               : (0x20002075ull | (uint64_t('0' + k1) << 16));
-        const int pl = two ? 5 : 4;
-        int d;
-        const uint64_t D = dec8(s.lane[line - 3], d);
-        V = static_cast<u128>(P) | (static_cast<u128>(D) << (8 * pl)) | (static_cast<u128>('\n') << (8 * (pl + d)));
-        return pl + d + 1;
-    }
+// Header line `line` (0..2) of serialize.hpp:21-27 as bytes of a u128 (byte 0
+// first): 0 "ranmar24 v1", 1 "i <i+1> j <j+1>", 2 "v <v>", each with its
+// '\n'. (Dx, dx) is dec8 of the line's first number (i + 1 or v), computed
+// with the other lanes' lane values; j + 1 <= 97 takes one division.
+// Returns the length (<= 14).
+__device__ __forceinline__ int format_header(const ranmar_state& s, int line, uint64_t Dx, int dx, u128& V) {
     if (line == 0) {  // "ranmar24 v1\n"
         V = static_cast<u128>(0x343272616D6E6172ull) | (static_cast<u128>(0x0A317620ull) << 64);
         return 12;
     }
     if (line == 1) {  // "i a j b\n"
-        int da, db;
-        const uint64_t A = dec8(static_cast<uint32_t>(s.i + 1), da);
-        const uint64_t B = dec8(static_cast<uint32_t>(s.j + 1), db);
-        V = static_cast<u128>(0x2069u) | (static_cast<u128>(A) << 16) |
-            (static_cast<u128>(0x206A20u) << (16 + 8 * da)) | (static_cast<u128>(B) << (40 + 8 * da)) |
-            (static_cast<u128>('\n') << (40 + 8 * (da + db)));
-        return 6 + da + db;
+        const uint32_t j1 = static_cast<uint32_t>(s.j + 1), jt = j1 / 10u;
+        const int db = j1 >= 10u ? 2 : 1;
+        const uint64_t B = j1 >= 10u ? (('0' + jt) | (uint64_t('0' + j1 - 10u * jt) << 8)) : ('0' + j1);
+        V = static_cast<u128>(0x2069u) | (static_cast<u128>(Dx) << 16) |
+            (static_cast<u128>(0x206A20u | (B << 24) | (uint64_t('\n') << (24 + 8 * db))) << (16 + 8 * dx));
+        return 6 + dx + db;
     }
-    int d;  // "v x\n"
-    const uint64_t D = dec8(s.v, d);
-    V = static_cast<u128>(0x2076u) | (static_cast<u128>(D) << 16) | (static_cast<u128>('\n') << (16 + 8 * d));
-    return 3 + d;
+    V = static_cast<u128>(0x2076u) | (static_cast<u128>(Dx) << 16) | (static_cast<u128>('\n') << (16 + 8 * dx));
+    return 3 + dx;  // "v x\n"
 }
 
 // The len (<= 14) bytes of V at byte offset p of the zero-initialised stage
@@ -182,7 +168,9 @@ __global__ void __launch_bounds__(32 * kTTStates)
     for (int pass = 0; pass < 4; ++pass) {
         const int line = pass * 32 + l;
         const bool u = line >= 3 && line < 100;
-        x[pass] = inr && u ? s.lane[line - 3] : 0u;
+        // header lanes convert their first number with everyone else's
+        const uint32_t h = line == 1 ? static_cast<uint32_t>(s.i + 1) : line == 2 ? s.v : 0u;
+        x[pass] = !inr ? 0u : u ? s.lane[line - 3] : h;
         bad |= x[pass] > kMask;
     }
     bad = __any_sync(0xffffffffu, bad || (inr && l == 0 && !state_ok(s.i, s.j, s.v)));
@@ -201,7 +189,7 @@ __global__ void __launch_bounds__(32 * kTTStates)
         uint32_t len = 0;
         if (act && line < 100) {
             if (pass == 0 && l < 3)
-                len = static_cast<uint32_t>(format_line(s, line, V));
+                len = static_cast<uint32_t>(format_header(s, line, D[0], dg[0], V));
             else
                 len = u_line_len(static_cast<uint32_t>(line - 2), dg[pass]);
         }
@@ -440,6 +428,25 @@ __device__ __forceinline__ bool parse_num_fast(const uint32_t* S, int q, int L, 
     return true;
 }
 
+// Line 2 "i <a> j <b>" (serialize.hpp:98-105) with 1- or 2-digit numbers and
+// single spaces: true and (i, j) = (a, b), else false (the character-level
+// checks decide). Same values as the reference's take_uint on such a line.
+__device__ __forceinline__ bool parse_ij_fast(const uint32_t* S, int q, int L, uint64_t& i, uint64_t& j) {
+    if (L < 7 || L > 9) return false;
+    uint64_t lo, hi;
+    load16(S, q, lo, hi);
+    auto c = [&](int k) -> uint32_t { return static_cast<uint32_t>((k < 8 ? lo >> (8 * k) : hi >> (8 * (k - 8))) & 0xFF); };
+    auto dig = [](uint32_t ch) { return ch - '0' <= 9u; };
+    if ((lo & 0xFFFF) != 0x2069) return false;  // "i "
+    const int da = c(3) == ' ' ? 1 : 2, db = L - 5 - da;
+    if (db < 1 || db > 2 || c(2 + da) != ' ' || c(3 + da) != 'j' || c(4 + da) != ' ') return false;
+    const uint32_t a0 = c(2), a1 = c(3), b0 = c(5 + da), b1 = c(6 + da);
+    if (!dig(a0) || (da == 2 && !dig(a1)) || !dig(b0) || (db == 2 && !dig(b1))) return false;
+    i = da == 2 ? 10u * (a0 - '0') + (a1 - '0') : a0 - '0';
+    j = db == 2 ? 10u * (b0 - '0') + (b1 - '0') : b0 - '0';
+    return true;
+}
+
 // Line "u <k1> <x>" (serialize.hpp:115-126) in canonical form: 1 (x <= kMask,
 // lane = x), 0 (x > kMask: the reference fails on this line), -1 (not
 // canonical: the character-level checks decide).
@@ -544,12 +551,14 @@ __global__ void __launch_bounds__(32 * kFTWarps, 12)
                 }
             } else if (ln == 2) {
                 uint64_t i = 0, j = 0;
-                ok = en - p >= 2 && sm[p] == 'i' && sm[p + 1] == ' ';
-                p += 2;
-                ok = ok && num_at(sm, p, en, i);
-                ok = ok && en - p >= 3 && sm[p] == ' ' && sm[p + 1] == 'j' && sm[p + 2] == ' ';
-                p += 3;
-                ok = ok && num_at(sm, p, en, j) && p == en;
+                if (!parse_ij_fast(S, sh + p, en - p, i, j)) {
+                    ok = en - p >= 2 && sm[p] == 'i' && sm[p + 1] == ' ';
+                    p += 2;
+                    ok = ok && num_at(sm, p, en, i);
+                    ok = ok && en - p >= 3 && sm[p] == ' ' && sm[p + 1] == 'j' && sm[p + 2] == ' ';
+                    p += 3;
+                    ok = ok && num_at(sm, p, en, j) && p == en;
+                }
                 ok = ok && i >= 1 && i <= 97 && j >= 1 && j <= 97 && (i + 97 - j) % 97 == 64;
                 si = static_cast<int32_t>(i) - 1;
                 sj = static_cast<int32_t>(j) - 1;

@@ -132,6 +132,13 @@ def test_from_text_errors_match_reference(refvec):
         good.replace("ranmar24 v1", "Ranmar24 v1"),    # header case
         good.replace("ranmar24 v1", "ranmar24 v10"),   # header one byte long
         good.replace("ranmar24 v1", "ranmar24 v"),     # header one byte short
+        good.replace("i 97 j 33", "i 5 j 38"),         # one-digit i
+        good.replace("i 97 j 33", "i 72 j 8"),         # one-digit j
+        good.replace("i 97 j 33", "i 097 j 33"),       # i with a leading zero
+        good.replace("i 97 j 33", "i 97 j 3x"),        # letter in j
+        good.replace("i 97 j 33", "i 97  j 33"),       # double space
+        good.replace("i 97 j 33", "i 9x j 33"),        # letter in i
+        good.replace("i 97 j 33", "i 1 j 35"),         # separation off by one
     ]
     texts = [b.encode() for b in bad]
     offs = np.cumsum([0] + [len(t) for t in texts]).astype(np.int64)
@@ -141,7 +148,7 @@ def test_from_text_errors_match_reference(refvec):
     for k, b in enumerate(bad):
         assert err[k] == _host_error_line(b), (k, b[:40])
     ok = [k for k, e in enumerate(err) if e == 0]
-    assert ok == [11, 12, 14, 15, 17, 21, 22, 23, 25, 31, 35, 37, 38]
+    assert ok == [11, 12, 14, 15, 17, 21, 22, 23, 25, 31, 35, 37, 38, 43, 44, 45]
     host = rb.states_to_host(states)
     for k in ok:
         assert host[k:k + 1].tobytes() == rb.from_text(bad[k]).tobytes()
