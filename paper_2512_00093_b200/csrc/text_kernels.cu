@@ -146,8 +146,8 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
 // barrier the CTA's range is stored with aligned 16-B stores (the stage read
 // at the global offset's misalignment by funnel shifts; bytes only for the
 // unaligned head and tail). tile_status[] and *ticket start zeroed.
-__global__ void __launch_bounds__(32 * kTTStates)
-    to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n, uint64_t* __restrict__ off,
+__global__ void
+    __launch_bounds__(32 * kTTStates, 7) to_text_kernel(const ranmar_state* __restrict__ st, uint64_t n, uint64_t* __restrict__ off,
                    char* __restrict__ text, uint64_t* tile_status, uint32_t* ticket, uint32_t* status) {
     __shared__ __align__(16) char stage[kTTStage];
     __shared__ uint32_t warp_len[kTTStates], warp_base[kTTStates];
