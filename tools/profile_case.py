@@ -1,6 +1,6 @@
 """Small, ncu-friendly drivers for one BASELINE config each (1 GPU).
 
-    python tools/profile_case.py c2|c3|c4|c5|lang|bank|text|jump [--warmup W]
+    python tools/profile_case.py c1|c2|c3|c4|c5|lang|bank|text|jump [--warmup W]
 
 Runs W warm-up repetitions and one more of the config's GPU job, so an ncu
 capture with `-k regex:<kernel> -s W -c 1` lands on a warm launch.
@@ -19,12 +19,18 @@ import paper_2512_00093_b200 as rb  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["c2", "c3", "c4", "c5", "lang", "bank", "text", "jump"])
+    ap.add_argument("case", choices=["c1", "c2", "c3", "c4", "c5", "lang", "bank", "text", "jump"])
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--c4-streams", type=int, default=1 << 16)
     args = ap.parse_args()
     reps = args.warmup + 1
-    if args.case == "c2":
+    if args.case == "c1":
+        # one stream x 10^8 fp32 at full width (substreams by make_streams, re-joined)
+        s1 = rb.states_to_device(rb.init(12345)).cuda()
+        out = torch.empty(10**8, dtype=torch.float32, device="cuda")
+        for _ in range(reps):
+            rb.generate_single(s1, 10**8, "f32", out=out)
+    elif args.case == "c2":
         n, per = 65536, 65536
         st = torch.empty((n, 100), dtype=torch.int32, device="cuda")
         ws = torch.empty(rb.lib().ranmar_make_streams_workspace(n), dtype=torch.uint8, device="cuda")
