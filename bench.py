@@ -474,7 +474,12 @@ def run_ours(args, rank, world, local):
         ms1 = max_over_ranks(a.elapsed_time(b), world)
         extras["config1"] = {"workload": "one stream (seed 12345) x 10^8 fp32, split into 8,192-output "
                                          "substreams (make_streams) and re-joined; state ends as 10^8 x step()",
-                             "ms": ms1, "uniforms_per_s": n1 / (ms1 * 1e-3)}
+                             "ms": ms1, "uniforms_per_s": n1 / (ms1 * 1e-3),
+                             "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": n1 * 4 / (ms1 * 1e-3) / 1e9,
+                                          "peak": peak, "frac": n1 * 4 / (ms1 * 1e-3) / 1e9 / peak,
+                                          "peak_kind": f"{peak_kind} copy GB/s (MEASURED_PEAKS.json hbm_gbs)",
+                                          "algorithmic_per_unit": "4 B stored per uniform (the whole call: "
+                                                                  "substream starts, generation, re-join)"}}
         del out1
 
     # ---- config 3: 2^20 stream starts at J = 2^120 (jump-aheads/s) ----
@@ -574,7 +579,14 @@ def run_ours(args, rank, world, local):
             "workload": "to_text / from_text of config 3's 2^20 stream starts (reference text format)",
             "text_bytes": tb, "to_text_states_per_s": n3 * world / (ms_tt * 1e-3),
             "from_text_states_per_s": n3 * world / (ms_ft * 1e-3),
-            "to_text_ms": ms_tt, "from_text_ms": ms_ft}
+            "to_text_ms": ms_tt, "from_text_ms": ms_ft,
+            # algorithmic bytes: the states read + the text written (to_text), and back (from_text)
+            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                         "to_text_achieved": (tb + n3 * 400) / (ms_tt * 1e-3) / 1e9,
+                         "from_text_achieved": (tb + n3 * 400) / (ms_ft * 1e-3) / 1e9,
+                         "to_text_frac": (tb + n3 * 400) / (ms_tt * 1e-3) / 1e9 / peak,
+                         "from_text_frac": (tb + n3 * 400) / (ms_ft * 1e-3) / 1e9 / peak,
+                         "note": "both kernels are instruction-bound (character-level work), see DESIGN §3 K7"}}
         if world == 1 and not args.no_cpu:
             extras["persistence"]["cpu_reference"] = cpu_reference_text(rb.states_to_host(st3[:1 << 16]))
         del st3, ws3, jo, text, off, back, err
