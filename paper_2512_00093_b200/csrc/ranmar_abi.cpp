@@ -978,7 +978,12 @@ size_t ranmar_text_workspace(uint64_t n) { return rb::text_workspace(n); }
 
 int ranmar_to_text_dev(const ranmar_state* d_states, uint64_t n, char* d_text, uint64_t text_cap,
                        uint64_t* d_offsets, void* d_ws, size_t ws_bytes, void* stream) {
-    if (n == 0) return RANMAR_OK;
+    if (n == 0) {  // no texts: d_offsets[0] = 0 total bytes
+        if (d_offsets)
+            RB_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(uint64_t), static_cast<cudaStream_t>(stream)),
+                    "offsets memset");
+        return RANMAR_OK;
+    }
     if (!d_states || !d_text || !d_offsets || !d_ws) return fail(RANMAR_EINVAL, "ranmar: null device buffer");
     if (text_cap < rb::text_bound(n)) return fail(RANMAR_ENOMEM, "ranmar: text buffer below ranmar_to_text_bound(n)");
     if (ws_bytes < rb::text_workspace(n)) return fail(RANMAR_ENOMEM, "ranmar: workspace too small");

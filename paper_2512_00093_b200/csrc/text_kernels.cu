@@ -179,19 +179,22 @@ __global__ void
     // it: the shuffles then run in converged code.
     const bool act = inr && !bad;
     uint64_t D[4];
-    int dg[4];
+    int dx = 0;  // digits of the header lanes' first number (pass 0)
     uint32_t incl[4], tot = 0;
-    u128 V = 0;  // header line (pass 0, lanes 0..2)
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
         const int line = pass * 32 + l;
-        D[pass] = dec8(x[pass], dg[pass]);
+        int d;
+        D[pass] = dec8(x[pass], d);
+        if (pass == 0) dx = d;
         uint32_t len = 0;
         if (act && line < 100) {
-            if (pass == 0 && l < 3)
-                len = static_cast<uint32_t>(format_header(s, line, D[0], dg[0], V));
-            else
-                len = u_line_len(static_cast<uint32_t>(line - 2), dg[pass]);
+            if (pass == 0 && l < 3) {
+                u128 V;
+                len = static_cast<uint32_t>(format_header(s, line, D[0], d, V));
+            } else {
+                len = u_line_len(static_cast<uint32_t>(line - 2), d);
+            }
         }
         uint32_t y = len;
 #pragma unroll
@@ -225,10 +228,14 @@ __global__ void
         for (int pass = 0; pass < 4; ++pass) {
             const uint32_t len = incl[pass] >> 24, p = base + (incl[pass] & 0xFFFFFFu) - len;
             if (!len) continue;
-            if (pass == 0 && l < 3)
+            if (pass == 0 && l < 3) {  // the header line again (cheap, three lanes)
+                u128 V;
+                format_header(s, pass * 32 + l, D[0], dx, V);
                 emit_line(S, p, static_cast<int>(len), V);
-            else
-                emit_u_line(S, p, static_cast<uint32_t>(pass * 32 + l - 2), D[pass], dg[pass]);
+            } else {
+                const uint32_t k1 = static_cast<uint32_t>(pass * 32 + l - 2);
+                emit_u_line(S, p, k1, D[pass], static_cast<int>(len) - (k1 >= 10u ? 6 : 5));
+            }
         }
     }
     if (w == 0) {  // look-back for the tile's global offset

@@ -425,7 +425,7 @@ def test_zero_sized_calls_are_no_ops(oracle):
     gf = torch.zeros(2, dtype=torch.float64, device="cuda")
     rb.langevin(g[:0], f, f, torch.zeros(0, dtype=torch.int32, device="cuda"), gf, gf, 1.0)
     text, off = rb.to_text_dev(empty)
-    assert off.numel() == 1
+    assert off.numel() == 1 and int(off[0]) == 0 and rb.texts_to_host(text, off) == []
     torch.cuda.synchronize()
     assert rb.device_status() == 0
 
