@@ -147,13 +147,19 @@ def dist_setup(gpus: int, need_gpu: bool):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != gpus:
         raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world} ranks were launched")
+    # Test hook (never set by the driver): RANMAR_BENCH_SHARED_GPU=1 runs every rank on
+    # cuda:0 over gloo, so the N > 1 code path (shards, max over ranks, gathers) can be
+    # exercised on a one-GPU box; NCCL refuses two ranks on one device.
+    shared = os.environ.get("RANMAR_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if need_gpu and torch.cuda.device_count() < local + 1:
         raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
                          f"{torch.cuda.device_count()} CUDA device(s) visible")
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if torch.cuda.is_available() and not shared else "gloo")
     return rank, world, local
 
 
@@ -168,7 +174,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -695,7 +701,8 @@ def run_ours(args, rank, world, local):
         del mom5
         # after timing: every rank's deviate sum and sum of squares, all-gathered
         from paper_2512_00093_b200.shard import allgather_tensor
-        mom = torch.stack([out5.sum(dtype=torch.float64), (out5 * out5).sum(dtype=torch.float64)])
+        flat5 = out5.view(-1)  # (dot: no 40 GB temporary for the squares)
+        mom = torch.stack([flat5.sum(dtype=torch.float64), torch.dot(flat5, flat5)])
         mom = allgather_tensor(mom).view(-1, 2)
         cnt5 = out5.numel() * world
         extras["config5"]["gathered"] = {"mean": float(mom[:, 0].sum()) / cnt5,

@@ -25,6 +25,13 @@ def weak_range(n_per_rank: int, rank: int) -> Tuple[int, int]:
     return rank * n_per_rank, n_per_rank
 
 
+def _host_if_gloo(t):
+    """gloo's all_gather has no CUDA path: carry CUDA tensors through the host there
+    (NCCL, the multi-GPU backend, takes them as they are)."""
+    import torch.distributed as dist
+    return t.cpu() if t.is_cuda and dist.get_backend() == "gloo" else t
+
+
 def gather_u64(values: Sequence[int], device=None) -> List[List[int]]:
     """All-gather a short list of u64 checksums from every rank (torch.distributed;
     NCCL on GPUs, gloo on CPU). Values are carried as int64 bit patterns."""
@@ -38,6 +45,7 @@ def gather_u64(values: Sequence[int], device=None) -> List[List[int]]:
     t = torch.tensor([to_i64(v) for v in values], dtype=torch.int64, device=device)
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return [[v & ((1 << 64) - 1) for v in t.tolist()]]
+    t = _host_if_gloo(t)
     out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(out, t)
     return [[v & ((1 << 64) - 1) for v in o.tolist()] for o in out]
@@ -51,14 +59,18 @@ def allgather_tensor(t):
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return t
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, t.contiguous())
-    return torch.cat(out)
+    src = _host_if_gloo(t.contiguous())
+    out = [torch.empty_like(src) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, src)
+    return torch.cat(out).to(t.device)
 
 
 def allreduce_sum(t):
     """Sum-reduce a tensor over ranks in place (the 256-bin histogram total)."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        src = _host_if_gloo(t)
+        dist.all_reduce(src, op=dist.ReduceOp.SUM)
+        if src is not t:
+            t.copy_(src)
     return t
