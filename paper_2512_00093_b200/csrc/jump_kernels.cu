@@ -285,14 +285,39 @@ __global__ void __launch_bounds__(32 * kPowTabWarps)
 // (warp per entry); Tab_0 and Tab_1 also written transposed for the bulk kernels.
 // One CTA per entry: its <= 6 products run at CTA speed (the chain is the
 // latency of the whole setup, not the few MACs).
-// With put_dst set, block 0 also writes the host-given base state `put` to
-// put_dst (the launch that would otherwise be put_state_kernel's).
+// With put_dst set, block 0 also writes the base state to put_dst (the launch
+// that would otherwise be put_state_kernel's / copy_state_kernel's): the
+// host-given `put`, or, when dsrc is set, the device-resident *dsrc after the
+// invariant check (core.hpp:29-49; a bad state raises the status bit and is
+// replaced by a zero state, so nothing downstream reads out of range).
 __global__ void __launch_bounds__(256)
     tables_kernel(const uint32_t* __restrict__ Q, uint32_t* __restrict__ Tab,
                   uint32_t* __restrict__ Tt, const __grid_constant__ ranmar_state put,
-                  ranmar_state* __restrict__ put_dst) {
-    if (put_dst && blockIdx.x == 0 && threadIdx.x < 100)
-        reinterpret_cast<uint32_t*>(put_dst)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&put)[threadIdx.x];
+                  const ranmar_state* __restrict__ dsrc, ranmar_state* __restrict__ put_dst,
+                  uint32_t* status) {
+    if (put_dst && blockIdx.x == 0) {
+        const int k = threadIdx.x;
+        if (!dsrc) {
+            if (k < 100) reinterpret_cast<uint32_t*>(put_dst)[k] = reinterpret_cast<const uint32_t*>(&put)[k];
+        } else {
+            __shared__ int bad;
+            if (k == 0) bad = !state_ok(dsrc->i, dsrc->j, dsrc->v);
+            __syncthreads();
+            if (k < 97 && dsrc->lane[k] > kMask) bad = 1;
+            __syncthreads();
+            if (bad) {
+                if (k == 0) atomicOr(status, kStatusBadState);
+                if (k < 97) put_dst->lane[k] = 0;
+                if (k == 0) {
+                    put_dst->i = 96;
+                    put_dst->j = 32;
+                    put_dst->v = 0;
+                }
+            } else if (k < 100) {
+                reinterpret_cast<uint32_t*>(put_dst)[k] = reinterpret_cast<const uint32_t*>(dsrc)[k];
+            }
+        }
+    }
     __shared__ uint32_t f[7][kPolyN];  // the entry's factors, fetched together up front
     __shared__ uint32_t acc[kPolyN];
     __shared__ BlockMulScratch scr;
@@ -574,27 +599,6 @@ __global__ void __launch_bounds__(kApplyItems * (WMODE ? 25 : 13) * JS)
 // satisfy the reference's invariants. A bad state raises kStatusBadState and is
 // replaced by the all-zero state with fresh cursors, so no later kernel indexes
 // out of range.
-__global__ void copy_state_kernel(const ranmar_state* __restrict__ src, ranmar_state* __restrict__ dst,
-                                  uint32_t* status) {
-    __shared__ int bad;
-    const int k = threadIdx.x;
-    if (k == 0) bad = !state_ok(src->i, src->j, src->v);
-    __syncthreads();
-    if (k < 97 && src->lane[k] > kMask) bad = 1;
-    __syncthreads();
-    if (bad) {
-        if (k == 0) atomicOr(status, kStatusBadState);
-        if (k < 97) dst->lane[k] = 0;
-        if (k == 0) {
-            dst->i = 96;
-            dst->j = 32;
-            dst->v = 0;
-        }
-        return;
-    }
-    if (k < 100) reinterpret_cast<uint32_t*>(dst)[k] = reinterpret_cast<const uint32_t*>(src)[k];
-}
-
 // ---- make_streams bulk (level 0): s_{(first + 128 h + r) J} = apply(anchor_h, T_r).
 // Per anchor a 128 x 97 x 97 integer "GEMM" tile on the IMAD pipe:
 //  * T^T (97 x 128) stays in shared memory for every anchor the CTA visits;
@@ -1532,11 +1536,13 @@ cudaError_t launch_pow_table(const uint64_t (*e)[4], const int* shift, uint32_t*
 }
 
 cudaError_t launch_tables(const uint32_t* Q, int levels, uint32_t* Tab, uint32_t* Tt,
-                          const ranmar_state* put, ranmar_state* put_dst, cudaStream_t stream) {
+                          const ranmar_state* put, const ranmar_state* d_src, ranmar_state* put_dst,
+                          uint32_t* status, cudaStream_t stream) {
     count_launch();
     ranmar_state pv{};
     if (put) pv = *put;
-    tables_kernel<<<levels * kRows, 256, 0, stream>>>(Q, Tab, Tt, pv, put ? put_dst : nullptr);
+    tables_kernel<<<levels * kRows, 256, 0, stream>>>(Q, Tab, Tt, pv, put ? nullptr : d_src,
+                                                      put || d_src ? put_dst : nullptr, status);
     return cudaGetLastError();
 }
 
@@ -1605,12 +1611,6 @@ cudaError_t launch_level(const ranmar_state* in, uint64_t count, const uint32_t*
 }
 
 
-cudaError_t launch_copy_state(const ranmar_state* src, ranmar_state* dst, uint32_t* status,
-                              cudaStream_t stream) {
-    count_launch();
-    copy_state_kernel<<<1, 128, 0, stream>>>(src, dst, status);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_bulk(const uint32_t* W1, uint64_t H, const uint32_t* Tt, ranmar_state* out,
                         uint64_t first, uint64_t n, uint32_t jm, const ranmar_state* d_base,

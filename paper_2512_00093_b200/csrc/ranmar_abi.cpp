@@ -68,13 +68,12 @@ cudaError_t launch_crlog_sweep(uint64_t, uint64_t, int, unsigned long long*, uin
 cudaError_t launch_pow(const PowJobs&, int, cudaStream_t);
 cudaError_t launch_pow_table(const uint64_t (*)[4], const int*, uint32_t* const*, int,
                              const uint32_t*, cudaStream_t);
-cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, const ranmar_state*, ranmar_state*,
-                          cudaStream_t);
+cudaError_t launch_tables(const uint32_t*, int, uint32_t*, uint32_t*, const ranmar_state*,
+                          const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
 cudaError_t launch_apply(const ranmar_state*, ranmar_state*, uint64_t, const uint32_t*, uint32_t,
                          uint32_t*, int, cudaStream_t);
 cudaError_t launch_level(const ranmar_state*, uint64_t, const uint32_t*, uint32_t, ranmar_state*,
                          uint32_t*, uint32_t*, cudaStream_t);
-cudaError_t launch_copy_state(const ranmar_state*, ranmar_state*, uint32_t*, cudaStream_t);
 cudaError_t launch_level_tc(const uint32_t*, uint64_t, const uint32_t*, uint64_t, uint32_t,
                             const ranmar_state*, uint32_t*, uint32_t*, uint32_t*, int, cudaStream_t);
 cudaError_t launch_bulk(const uint32_t*, uint64_t, const uint32_t*, ranmar_state*, uint64_t,
@@ -551,7 +550,7 @@ int ranmar_jump_dev(const ranmar_state* d_in, ranmar_state* d_out, uint64_t n,
 namespace {
 
 // make_streams for a base state given on the host (h_base, checked here) or in
-// device memory (d_base, checked by copy_state_kernel, which flags the status
+// device memory (d_base, checked by tables_kernel, which flags the status
 // word): exactly one of them is non-null.
 int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
                       const ranmar_jump_count* j, uint64_t first, uint64_t n, ranmar_state* d_out,
@@ -621,12 +620,10 @@ int make_streams_impl(const ranmar_state* h_base, const ranmar_state* d_base,
     // Offset tables Tab_L[r] = P_{r 128^L J}.
     // (a host-given base state rides along as a kernel parameter and is written
     // into the workspace by the same launch)
-    RB_CUDA(rb::launch_tables(Qsrc, p.tab_levels, Tab, Tt, h_base, dbase, s), "tables_kernel launch");
-    // The base state, in the workspace (a host-given one was written by tables_kernel);
-    // A_0 = s_{first J}.
-    if (!h_base) {
-        RB_CUDA(rb::launch_copy_state(d_base, dbase, status, s), "copy_state launch");
-    }
+    // The base state goes into the workspace with the same launch (a device-resident
+    // one checked there); A_0 = s_{first J}.
+    RB_CUDA(rb::launch_tables(Qsrc, p.tab_levels, Tab, Tt, h_base, d_base, dbase, status, s),
+            "tables_kernel launch");
     const uint32_t jm = mod_u32(J, kMod);
     const ranmar_state* a0 = dbase;
     if (first > 0) {
