@@ -141,16 +141,56 @@ __device__ __forceinline__ double convert_out<double>(uint32_t raw) {
 
 constexpr int kGenWarps = 8;  // streams per 256-thread block
 
+// The last stream's state re-laid into the ORIGINAL ring layout of *dst, i.e.
+// exactly what `count` calls of step() leave on one stream generated as
+// substreams (ranmar_generate_single_*): canonical u[k] = lane[(i - k) mod 97]
+// is layout-independent, and lane[(i_t - k) mod 97] = u[k] with the target
+// cursor i_t = (i0 - count) mod 97 (jump.hpp:32-48). i0 is read from dst (the
+// original state) before it is overwritten; an invalid original state was
+// already flagged by make_streams and is left untouched. One warp.
+__device__ __forceinline__ void warp_relayout(const ranmar_state* __restrict__ src,
+                                              ranmar_state* __restrict__ dst, int count_mod97) {
+    const int l = threadIdx.x & 31;
+    const int i0 = dst->i;
+    const bool ok = state_ok(i0, dst->j, dst->v);
+    const int i_t = (i0 - count_mod97 + 97) % 97, si = src->i;
+    const uint32_t sv = src->v;
+    __syncwarp();  // every lane has read dst's cursors before lane 0 rewrites them
+    if (!ok) return;
+    for (int k = l; k < 97; k += 32) {
+        int q = si - k;
+        q += q < 0 ? 97 : 0;
+        int r = i_t - k;
+        r += r < 0 ? 97 : 0;
+        dst->lane[r] = src->lane[q];
+    }
+    if (l == 0) {
+        dst->i = i_t;
+        dst->j = i_t >= 64 ? i_t - 64 : i_t + 33;
+        dst->v = sv;
+    }
+}
+
+// Warp per stream. per_last = the last stream's output count (per_stream for a
+// plain launch); with relay set, the last stream's warp also re-lays its final
+// state into *relay (ranmar_generate_single_*: the substreams' tail and the
+// re-join ride in the same launch).
 template <class T>
 __global__ void __launch_bounds__(32 * kGenWarps)
     gen_store_kernel(ranmar_state* __restrict__ states, uint64_t n_streams, uint64_t per_stream,
-                     T* __restrict__ out, uint32_t* status) {
+                     T* __restrict__ out, uint32_t* status, uint64_t per_last,
+                     ranmar_state* __restrict__ relay, int count_mod97) {
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kGenWarps + (threadIdx.x >> 5);
     if (k >= n_streams) return;
+    const bool last = k == n_streams - 1;
     T* o = out + k * per_stream + (threadIdx.x & 31);
-    warp_stream(states + k, per_stream, status, [&](uint64_t r, uint32_t raw, bool valid) {
+    warp_stream(states + k, last ? per_last : per_stream, status, [&](uint64_t r, uint32_t raw, bool valid) {
         if (valid) st_cs(o + 32 * r, convert_out<T>(raw));
     });
+    if (relay && last) {
+        __syncwarp();  // the stream's state, stored by its lanes, is visible to the warp
+        warp_relayout(states + k, relay, count_mod97);
+    }
 }
 
 // Trace of N steps per stream (the scalar step() of the C++ facade): u[n] =
@@ -177,48 +217,9 @@ __global__ void __launch_bounds__(32 * kGenWarps)
     g.store(states + k, per_stream, rounds);
 }
 
-// One stream generated as P substreams (ranmar_generate_single_*): the final
-// state is the last substream's, re-laid in the ORIGINAL ring layout, i.e.
-// exactly what `count` calls of step() leave: canonical u[k] = lane[(i - k)
-// mod 97] is layout-independent, and lane[(i_t - k) mod 97] = u[k] with the
-// target cursor i_t = (i0 - count) mod 97 (jump.hpp:32-48). i0 is read from
-// dst (the original state) before it is overwritten; an invalid original state
-// was already flagged by make_streams and is left untouched.
-__global__ void relayout_kernel(const ranmar_state* __restrict__ src, ranmar_state* __restrict__ dst,
-                                int count_mod97) {
-    __shared__ int s_it;
-    const int k = threadIdx.x;
-    if (k == 0) {
-        const int i0 = dst->i;
-        s_it = state_ok(i0, dst->j, dst->v) ? (i0 - count_mod97 + 97) % 97 : -1;
-    }
-    __syncthreads();
-    const int i_t = s_it;
-    if (i_t < 0) return;
-    if (k < 97) {
-        int q = src->i - k;
-        q += q < 0 ? 97 : 0;
-        int r = i_t - k;
-        r += r < 0 ? 97 : 0;
-        dst->lane[r] = src->lane[q];
-    }
-    if (k == 0) {
-        dst->i = i_t;
-        dst->j = i_t >= 64 ? i_t - 64 : i_t + 33;
-        dst->v = src->v;
-    }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-
-cudaError_t launch_relayout(const ranmar_state* src, ranmar_state* dst, int count_mod97,
-                            cudaStream_t stream) {
-    count_launch();
-    relayout_kernel<<<1, 128, 0, stream>>>(src, dst, count_mod97);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_generate_trace(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
                                   uint32_t* d_u, uint32_t* d_x, uint32_t* d_v, uint32_t* status,
@@ -232,20 +233,37 @@ cudaError_t launch_generate_trace(ranmar_state* d_states, uint64_t n_streams, ui
 }
 
 template <class T>
+cudaError_t launch_generate_joined(ranmar_state*, uint64_t, uint64_t, uint64_t, T*, ranmar_state*, int,
+                                   uint32_t*, cudaStream_t);
+
+template <class T>
 cudaError_t launch_generate(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
                             T* d_out, uint32_t* status, cudaStream_t stream) {
+    return launch_generate_joined<T>(d_states, n_streams, per_stream, per_stream, d_out, nullptr, 0,
+                                     status, stream);
+}
+
+// n_streams substreams of per_stream outputs, the last one per_last, in one
+// launch; with relay set the last substream's final state is re-laid into it.
+template <class T>
+cudaError_t launch_generate_joined(ranmar_state* d_states, uint64_t n_streams, uint64_t per_stream,
+                                   uint64_t per_last, T* d_out, ranmar_state* relay, int count_mod97,
+                                   uint32_t* status, cudaStream_t stream) {
     if (n_streams == 0) return cudaSuccess;
     const uint64_t blocks = (n_streams + kGenWarps - 1) / kGenWarps;
     count_launch();
     gen_store_kernel<T><<<static_cast<unsigned>(blocks), 32 * kGenWarps, 0, stream>>>(
-        d_states, n_streams, per_stream, d_out, status);
+        d_states, n_streams, per_stream, d_out, status, per_last, relay, count_mod97);
     return cudaGetLastError();
 }
-template cudaError_t launch_generate<uint32_t>(ranmar_state*, uint64_t, uint64_t, uint32_t*,
-                                               uint32_t*, cudaStream_t);
-template cudaError_t launch_generate<float>(ranmar_state*, uint64_t, uint64_t, float*, uint32_t*,
-                                            cudaStream_t);
-template cudaError_t launch_generate<double>(ranmar_state*, uint64_t, uint64_t, double*,
-                                             uint32_t*, cudaStream_t);
+#define RB_GEN_INST(T)                                                                                \
+    template cudaError_t launch_generate<T>(ranmar_state*, uint64_t, uint64_t, T*, uint32_t*,        \
+                                            cudaStream_t);                                          \
+    template cudaError_t launch_generate_joined<T>(ranmar_state*, uint64_t, uint64_t, uint64_t, T*, \
+                                                   ranmar_state*, int, uint32_t*, cudaStream_t);
+RB_GEN_INST(uint32_t)
+RB_GEN_INST(float)
+RB_GEN_INST(double)
+#undef RB_GEN_INST
 
 }  // namespace rb

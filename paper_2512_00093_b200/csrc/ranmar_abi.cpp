@@ -61,7 +61,9 @@ cudaError_t launch_bank_to_states(const uint32_t*, uint64_t, uint64_t, ranmar_st
 cudaError_t launch_langevin_bank(uint32_t*, uint64_t, uint64_t, const double*, double*,
                                  const int32_t*, const double*, const double*, int32_t, double,
                                  uint32_t*, cudaStream_t);
-cudaError_t launch_relayout(const ranmar_state*, ranmar_state*, int, cudaStream_t);
+template <class T>
+cudaError_t launch_generate_joined(ranmar_state*, uint64_t, uint64_t, uint64_t, T*, ranmar_state*, int,
+                                   uint32_t*, cudaStream_t);
 cudaError_t launch_fp64_selfcheck(uint64_t, uint64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_crlog_sweep(uint64_t, uint64_t, int, unsigned long long*, uint64_t*, uint64_t,
                                cudaStream_t);
@@ -739,11 +741,12 @@ int generate_single(ranmar_state* d_state, uint64_t count, T* d_out, void* d_ws,
     if (int rc = make_streams_impl(nullptr, d_state, &J, 0, parts, sub, ws2,
                                    ws_bytes - single_ws_states(parts), stream))
         return rc;
-    if (int rc = gen(sub, parts - 1, kSingleL, d_out, stream)) return rc;
+    // all substreams (the last one shorter) and the re-join into *d_state: one launch
     const uint64_t last = count - (parts - 1) * kSingleL;
-    if (int rc = gen(sub + parts - 1, 1, last, d_out + (parts - 1) * kSingleL, stream)) return rc;
-    RB_CUDA(rb::launch_relayout(sub + parts - 1, d_state, static_cast<int>(count % 97), s),
-            "relayout_kernel launch");
+    RB_STATUS_PTR(status);
+    RB_CUDA(rb::launch_generate_joined<T>(sub, parts, kSingleL, last, d_out, d_state,
+                                          static_cast<int>(count % 97), status, s),
+            "gen_store_kernel launch");
     return RANMAR_OK;
 }
 
