@@ -701,8 +701,10 @@ def run_ours(args, rank, world, local):
         del mom5
         # after timing: every rank's deviate sum and sum of squares, all-gathered
         from paper_2512_00093_b200.shard import allgather_tensor
-        flat5 = out5.view(-1)  # (dot: no 40 GB temporary for the squares)
-        mom = torch.stack([flat5.sum(dtype=torch.float64), torch.dot(flat5, flat5)])
+        # squares by chunked dots (no 40 GB temporary; BLAS dot takes < 2^31 elements)
+        flat5 = out5.view(-1)
+        sq5 = sum(torch.dot(c, c) for c in flat5.split(1 << 30))
+        mom = torch.stack([flat5.sum(dtype=torch.float64), sq5])
         mom = allgather_tensor(mom).view(-1, 2)
         cnt5 = out5.numel() * world
         extras["config5"]["gathered"] = {"mean": float(mom[:, 0].sum()) / cnt5,
