@@ -569,15 +569,19 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         assert int(err.abs().sum()) == 0 and torch.equal(back, st3)
         tb = int(off[-1].item())
+        ttw = torch.empty(int(rb.lib().ranmar_text_workspace(n3)), dtype=torch.uint8, device=dev)
+        tt_text, tt_off = torch.empty_like(text), torch.empty_like(off)  # buffers reused per call
+        rb.to_text_dev(st3, stream=stream, text=tt_text, offsets=tt_off, workspace=ttw)
         a.record(stream)
         for _ in range(reps):
-            rb.to_text_dev(st3, stream=stream)
+            rb.to_text_dev(st3, stream=stream, text=tt_text, offsets=tt_off, workspace=ttw)
         b.record(stream)
         torch.cuda.synchronize()
         ms_tt = max_over_ranks(a.elapsed_time(b) / reps, world)
+        ft_out, ft_err = torch.empty_like(back), torch.empty_like(err)
         a.record(stream)
         for _ in range(reps):
-            rb.from_text_dev(text, off, stream=stream)
+            rb.from_text_dev(text, off, stream=stream, out=ft_out, err=ft_err)
         b.record(stream)
         torch.cuda.synchronize()
         ms_ft = max_over_ranks(a.elapsed_time(b) / reps, world)
@@ -595,7 +599,7 @@ def run_ours(args, rank, world, local):
                          "note": "both kernels are instruction-bound (character-level work), see DESIGN §3 K7"}}
         if world == 1 and not args.no_cpu:
             extras["persistence"]["cpu_reference"] = cpu_reference_text(rb.states_to_host(st3[:1 << 16]))
-        del st3, ws3, jo, text, off, back, err
+        del st3, ws3, jo, text, off, back, err, tt_text, tt_off, ttw, ft_out, ft_err
 
     # ---- config 4: consume in kernel (no store) ----
     settle()

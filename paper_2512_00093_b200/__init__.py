@@ -569,28 +569,36 @@ def gaussian_stream(gstates, count: int, out=None, stream=None):
 
 
 @_on_device
-def to_text_dev(states, stream=None):
+def to_text_dev(states, stream=None, text=None, offsets=None, workspace=None):
     """Bulk ranmar::to_text (serialize.hpp:21-40) on the GPU.
-    Returns (text: uint8 CUDA tensor, offsets: int64 CUDA tensor [n + 1])."""
+    Returns (text: uint8 CUDA tensor, offsets: int64 CUDA tensor [n + 1]); text /
+    offsets / workspace may be passed in (sizes: ranmar_to_text_bound(n), n + 1,
+    ranmar_text_workspace(n) bytes) to reuse buffers across calls."""
     torch = _torch()
     n = states.shape[0]
-    text = torch.empty(int(lib().ranmar_to_text_bound(n)), dtype=torch.uint8, device="cuda")
-    off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
-    ws = torch.empty(int(lib().ranmar_text_workspace(n)), dtype=torch.uint8, device="cuda")
+    text = torch.empty(int(lib().ranmar_to_text_bound(n)), dtype=torch.uint8, device="cuda") if text is None else text
+    off = torch.empty(n + 1, dtype=torch.int64, device="cuda") if offsets is None else offsets
+    ws = (torch.empty(int(lib().ranmar_text_workspace(n)), dtype=torch.uint8, device="cuda")
+          if workspace is None else workspace)
+    if off.numel() != n + 1 or off.dtype != torch.int64:
+        raise ValueError("offsets must be an int64 tensor of n + 1 entries")
     _check(lib().ranmar_to_text_dev(_dptr(states), n, _dptr(text), text.numel(), _dptr(off),
                                     _dptr(ws), ws.numel(), _stream_ptr(stream)))
     return text, off
 
 
 @_on_device
-def from_text_dev(text, offsets, stream=None):
+def from_text_dev(text, offsets, stream=None, out=None, err=None):
     """Bulk ranmar::from_text (serialize.hpp:81-136) on the GPU: texts
     [offsets[k], offsets[k+1]) of `text` -> (states [n, 100], err [n]); err[k]
-    is 0 or the 1-based line where the reference's parser throws."""
+    is 0 or the 1-based line where the reference's parser throws (states[k] is
+    left as it was then: zeros unless `out` is passed in for reuse)."""
     torch = _torch()
     n = offsets.shape[0] - 1
-    states = torch.zeros((n, STATE_WORDS), dtype=torch.int32, device="cuda")
-    err = torch.empty(n, dtype=torch.int32, device="cuda")
+    states = torch.zeros((n, STATE_WORDS), dtype=torch.int32, device="cuda") if out is None else out
+    err = torch.empty(n, dtype=torch.int32, device="cuda") if err is None else err
+    if states.shape != (n, STATE_WORDS) or states.dtype != torch.int32 or err.numel() != n:
+        raise ValueError("out must be an int32 [n, 100] tensor and err an int32 [n] tensor")
     _check(lib().ranmar_from_text_dev(_dptr(text), _dptr(offsets), n, _dptr(states), _dptr(err),
                                       _stream_ptr(stream)))
     return states, err
